@@ -1,0 +1,218 @@
+/*
+ * skh.h -- C ABI of libskh.so: the s-hashing sketch hot path of Ski-LLS
+ * (Cartis, Fiala & Shao, "Hashing embeddings of optimal dimension, with
+ * applications to linear least squares", arXiv 2105.11815) on NVIDIA B200
+ * (sm_100a).
+ *
+ * The operation is Step 1 of the paper's Algorithm 1:
+ *   "Randomly draw a sketching matrix S in R^{m x n} ..., compute the
+ *    matrix-matrix product SA in R^{m x d} and the matrix-vector product
+ *    Sb in R^m",
+ * with S an s-hashing matrix (Def. def::sampling_and_hashing, L269-272:
+ * "independently for each j in [n], we sample without replacement
+ * i_1..i_s in [m] uniformly at random and let S_{i_k j} = +-1/sqrt(s)"), or the
+ * hashed randomised Hadamard transform S = S_h H D (Def. def::HRHT, L790-801:
+ * D random +-1 diagonal, H_ij = n^{-1/2} (-1)^{<(i-1)_2,(j-1)_2>}).
+ * Line numbers are PAPER.md lines; DESIGN.md §3 lists the readings (R1...)
+ * where the paper is silent (the random generator, index base, rounding order).
+ *
+ * Conventions for every entry point
+ *  - Pointers named *_host are HOST pointers (pinned memory recommended); every
+ *    other array pointer is a DEVICE pointer of the current CUDA device.  All
+ *    buffers are owned by the caller.  The library never allocates device
+ *    memory: scratch space is the caller-supplied workspace `ws` of at least the
+ *    size returned by the matching *_workspace_bytes query, 256-byte aligned.
+ *  - Matrices are row-major fp64 with a leading dimension (elements between the
+ *    starts of consecutive rows) >= the row length.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Device-pointer calls only enqueue work on `stream` and never synchronise;
+ *    outputs are valid once the stream reaches that point.  The *_host calls
+ *    enqueue their copies on `stream` too and return immediately; the caller
+ *    synchronises `stream` before reading the host outputs.
+ *  - Outputs are a pure function of the inputs and are bitwise reproducible run
+ *    to run (no floating-point atomics; every sum has a fixed order).
+ *  - Return value: SKH_OK (0) or one of the error codes below; on error nothing
+ *    has been enqueued, except SKH_ECUDA which reports a failed launch.
+ *    skh_last_error() returns a thread-local message for the last failure.
+ *  - Safe to call concurrently from several host threads on different streams
+ *    with different workspaces.
+ */
+#ifndef SKH_H_
+#define SKH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SKH_OK = 0,
+  SKH_EINVAL = 1,      /* n < 0, m < 1, d < 1, s < 1, s > m, s > 64, NULL required pointer */
+  SKH_ENOTPOW2 = 2,    /* skh_rht_stages: nrows not a multiple of 2^bit_hi            */
+  SKH_EDIM = 3,        /* lda/ldsa/ldx/ldy < d, Sb NULL while b given, bad row map      */
+  SKH_ERETRY = 4,      /* reserved: rejection-attempt cap reached (see skh_hash_gen)   */
+  SKH_EOVERFLOW = 5,   /* nrows * s >= 2^31 or m >= 2^31 (int32 indices)              */
+  SKH_EWORKSPACE = 6,  /* ws NULL or smaller than the *_workspace_bytes query         */
+  SKH_ECUDA = 7        /* a CUDA launch or copy failed (detail in skh_last_error())    */
+};
+
+/* Static description of an error code. */
+const char* skh_strerror(int code);
+/* Thread-local message describing the last failing call on this thread. */
+const char* skh_last_error(void);
+/* ABI version, currently 1. */
+int skh_abi_version(void);
+
+/* ------------------------------------------------------------------------ *
+ * Scale constants (R5, R9, R10).  Each is one IEEE sqrt followed by
+ * one IEEE divide in double precision, exactly as the CPU oracle computes it.
+ *   skh_c_s(s)        = 1 / sqrt(s)          entry magnitude of S  (L270)
+ *   skh_c_n(n_pad)    = 1 / sqrt(n_pad)      normalisation of H     (L796)
+ *   skh_c_ns(n_pad,s) = 1 / sqrt(n_pad * s)  S_h H applied once at the end
+ * ------------------------------------------------------------------------ */
+double skh_c_s(int32_t s);
+double skh_c_n(int64_t n_pad);
+double skh_c_ns(int64_t n_pad, int32_t s);
+
+/* ------------------------------------------------------------------------ *
+ * R1 + R2: draw S_h and transpose it into bucket lists.
+ *
+ * Draws the columns of S (= rows of A) held by this caller and builds the
+ * bucket lists, i.e. the CSR form of S restricted to those columns.  Local
+ * column k in [0, nrows) is global column
+ *     j(k) = row0 + (k / blk) * stride + (k % blk)      (blk <= 0: j(k) = row0 + k)
+ * which must be strictly increasing in k (stride >= blk); it covers contiguous
+ * row shards and the strided layout after a butterfly all-to-all.
+ *
+ * Column j's s rows are drawn by rejection (R1-R4): attempt
+ * t = 0, 1, ... draws r_t = floor(u(key, j*2^16 + t) * m / 2^64) with
+ * u = splitmix64 output stream keyed by mix64(seed ^ 0x48415348), accepted if
+ * not already drawn for j; the k-th accepted row has sign -1 iff bit k of
+ * u(key, j*2^16 + 0xFFFF) is set.
+ *
+ * Outputs (device, caller-owned):
+ *   col_rows  [nrows*s] int32  (nullable) bucket of the k-th draw of local col
+ *   col_signs [nrows*s] int8   (nullable) its sign (+1/-1), acceptance order
+ *   bucket_ptr  [m+1]   int32  bucket b's entries are [bucket_ptr[b], bucket_ptr[b+1])
+ *   bucket_rows [nrows*s] int32  LOCAL column k of each entry, ascending in each bucket
+ *   bucket_signs[nrows*s] int8   its sign
+ * The bucket lists are unique (a column hits a bucket at most once), so they are
+ * compared bit-exactly with the oracle.  nrows == 0 gives bucket_ptr = 0.
+ * The attempt cap (2^16 - 1 attempts per column) cannot be reached for s <= m
+ * in practice; if it were, the column keeps fewer than s entries and
+ * skh_hash_status() reports SKH_ERETRY.
+ * ------------------------------------------------------------------------ */
+size_t skh_hash_workspace_bytes(int64_t nrows, int64_t m, int32_t s);
+int skh_hash_gen(uint64_t seed, int64_t m, int32_t s,
+                 int64_t nrows, int64_t row0, int64_t blk, int64_t stride,
+                 int32_t* col_rows, int8_t* col_signs,
+                 int32_t* bucket_ptr, int32_t* bucket_rows, int8_t* bucket_signs,
+                 void* ws, size_t ws_bytes, void* stream);
+/* Synchronises `stream` and returns SKH_OK or SKH_ERETRY for the last
+ * skh_hash_gen that used workspace `ws`. */
+int skh_hash_status(const void* ws, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * R5, dense: SA = alpha * S A,  Sb = alpha * S b  (Alg. 1 Step 1, L871).
+ *
+ *   SA[bk, c] = alpha * ( ... ((0 + sg_1 A[r_1, c]) + sg_2 A[r_2, c]) + ... )
+ * over bucket bk's list in ascending local row (R10: the order of the
+ * oracle, so results are bit-identical to it).  alpha = skh_c_s(s) gives S A;
+ * alpha = 1 gives the unscaled signed sums used for sharded partials.
+ *   A  [nrows x d], lda >= d;  b [nrows] (nullable);  SA [m x d], ldsa >= d;
+ *   Sb [m] (required iff b != NULL).  SA/Sb must not alias A/b.
+ * `s` is only validated (1 <= s <= m); the lists define S.
+ * ------------------------------------------------------------------------ */
+int skh_sketch_dense(int64_t m, int32_t s,
+                     const int32_t* bucket_ptr, const int32_t* bucket_rows,
+                     const int8_t* bucket_signs,
+                     int64_t nrows, int64_t d, const double* A, int64_t lda,
+                     const double* b, double* SA, int64_t ldsa, double* Sb,
+                     double alpha, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * R5, sparse: SA (dense m x d) and Sb for A in CSR form, same
+ * summation order as skh_sketch_dense applied to the rows of A.
+ *   row_ptr [nrows+1] int64, col_idx [nnz] int32 (distinct within a row, each
+ *   < d), val [nnz] f64.  Column indices need not be sorted.
+ * ------------------------------------------------------------------------ */
+int skh_sketch_csr(int64_t m, int32_t s,
+                   const int32_t* bucket_ptr, const int32_t* bucket_rows,
+                   const int8_t* bucket_signs,
+                   int64_t nrows, int64_t d, const int64_t* row_ptr,
+                   const int32_t* col_idx, const double* val,
+                   const double* b, double* SA, int64_t ldsa, double* Sb,
+                   double alpha, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * R3 + R4: Y = alpha * Hhat_[bit_lo,bit_hi) (D?) X along the row index.
+ *
+ * For every column, the unnormalised radix-2 Walsh-Hadamard butterflies
+ * (x_i, x_{i+h}) <- (x_i + x_{i+h}, x_i - x_{i+h}), h = 2^bit, are applied for
+ * bit = bit_lo, ..., bit_hi - 1 in that order (R9) to the local row
+ * index i in [0, nrows).  With bit_lo = 0, bit_hi = log2(nrows), apply_diag = 1
+ * and alpha = skh_c_n(nrows) this is H D X of Def. def::HRHT (L790-801).
+ *   apply_diag: multiply local row i by D_{row0+i} before the first stage,
+ *     D_g = -1 iff bit (g & 63) of u(mix64(seed ^ 0x44494147), g >> 6) is set
+ *     (R7); rows i >= nvalid are read as zero (zero padding, R8).
+ *   X [nvalid x d] (ldx >= d), Y [nrows x d] (ldy >= d); Y may alias X
+ *   (then nvalid must equal nrows).  nrows must be a multiple of 2^bit_hi.
+ *   ws: scratch for the D bitmap, skh_rht_stages_workspace_bytes(nvalid, row0)
+ *   bytes (may be NULL when apply_diag == 0).
+ * ------------------------------------------------------------------------ */
+size_t skh_rht_stages_workspace_bytes(int64_t nvalid, int64_t row0);
+int skh_rht_stages(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0,
+                   int64_t d, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                   int bit_lo, int bit_hi, int apply_diag, double alpha,
+                   void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * R1-R5 on one GPU: SA = S_h H D A, Sb = S_h H D b (HRHT, Def. def::HRHT).
+ * n is padded to n_pad = 2^ceil(log2 n) with zero rows; S_h hashes all n_pad
+ * columns (R8).  SA[bk, :] = skh_c_ns(n_pad, s) * (ascending-row
+ * signed sum of the rows of Hhat D [A; 0]) -- bit-identical to the oracle.
+ *   A [n x d] (lda >= d), b [n] nullable, SA [m x d] (ldsa >= d), Sb [m].
+ * ------------------------------------------------------------------------ */
+size_t skh_rht_dense_workspace_bytes(int64_t n, int64_t m, int32_t s, int64_t d);
+int skh_rht_dense(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d,
+                  const double* A, int64_t lda, const double* b,
+                  double* SA, int64_t ldsa, double* Sb,
+                  void* ws, size_t ws_bytes, void* stream);
+
+/* Same computation from HOST buffers: A_host/b_host (pinned recommended) are
+ * copied to the device in row chunks whose transfer overlaps the first
+ * transform pass; SA_host/Sb_host receive the result.  Enqueued on `stream`;
+ * synchronise it before reading SA_host.  Workspace: the same query. */
+int skh_rht_dense_host(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d,
+                       const double* A_host, int64_t lda, const double* b_host,
+                       double* SA_host, int64_t ldsa, double* Sb_host,
+                       void* ws, size_t ws_bytes, void* stream);
+
+/* Plain s-hashing from HOST buffers (dense A): hash, copy A in chunks
+ * overlapped with nothing else to do, gather, copy SA/Sb back. */
+size_t skh_sketch_dense_workspace_bytes(int64_t n, int64_t m, int32_t s, int64_t d);
+int skh_sketch_dense_host(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d,
+                          const double* A_host, int64_t lda, const double* b_host,
+                          double* SA_host, int64_t ldsa, double* Sb_host,
+                          void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * Elementwise helper for sharded use: X[r, c] *= alpha for r < rows, c < cols.
+ * ------------------------------------------------------------------------ */
+int skh_scale(double* X, int64_t rows, int64_t cols, int64_t ldx, double alpha,
+              void* stream);
+
+/* Deterministic ordered sum of G partial blocks laid out consecutively:
+ * out[r, c] = (((P_0[r,c] + P_1[r,c]) + P_2[r,c]) + ...) * alpha, where
+ * P_g = parts + g * part_stride (elements), each [rows x cols] with ld `ldp`.
+ * Used after an all-to-all of SA strips (rank-order reduction). */
+int skh_ordered_sum(const double* parts, int64_t G, int64_t part_stride,
+                    int64_t rows, int64_t cols, int64_t ldp,
+                    double* out, int64_t ldo, double alpha, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKH_H_ */

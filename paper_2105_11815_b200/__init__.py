@@ -1,0 +1,8 @@
+"""B200-native s-hashing sketch hot path of Ski-LLS (arXiv 2105.11815).
+
+The product is libskh.so (CUDA kernels for sm_100a behind the C ABI in
+include/skh.h); this package is its thin Python binding (``api``) plus the
+multi-GPU sequencing (``sharded``).  See DESIGN.md.
+"""
+from .api import (BucketLists, RhtDense, SketchDenseHost, c_n, c_ns, c_s, hash_gen, hash_status,  # noqa: F401
+                  ordered_sum, rht_dense, rht_stages, scale, sketch_csr, sketch_dense)

@@ -1,0 +1,232 @@
+"""Python binding of libskh (same names as the C ABI in include/skh.h, minus
+the ``skh_`` prefix).  Argument marshalling only: every step of the path runs
+in the CUDA kernels behind the C ABI; torch supplies device memory and the
+current stream.  Raises on a missing library or non-CUDA tensors.
+
+Citations (PAPER.md lines): Alg. 1 Step 1 L871; s-hashing L269-272; HRHT
+L790-801.
+"""
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+
+def _stream():
+    return ctypes_ptr(torch.cuda.current_stream().cuda_stream)
+
+
+def ctypes_ptr(x):
+    return None if x is None else int(x)
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("libskh takes CUDA tensors (no CPU fallback)")
+
+
+def _ld(t):
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError("expected a row-major 2-D tensor with unit column stride")
+    return t.stride(0)
+
+
+def _workspace(nbytes, device):
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def c_s(s):
+    return _lib.load().skh_c_s(int(s))
+
+
+def c_n(n_pad):
+    return _lib.load().skh_c_n(int(n_pad))
+
+
+def c_ns(n_pad, s):
+    return _lib.load().skh_c_ns(int(n_pad), int(s))
+
+
+@dataclass
+class BucketLists:
+    """CSR form of S_h over this caller's columns (include/skh.h, skh_hash_gen)."""
+    m: int
+    s: int
+    nrows: int
+    ptr: torch.Tensor      # int32 [m+1]
+    rows: torch.Tensor     # int32 [nrows*s], local column ids
+    signs: torch.Tensor    # int8  [nrows*s]
+    col_rows: torch.Tensor = None
+    col_signs: torch.Tensor = None
+    ws: torch.Tensor = None
+
+
+def hash_gen(seed, m, s, nrows, row0=0, blk=0, stride=0, want_cols=False, device=None, out=None):
+    """R1+R2: draw the s-hashing columns j(k) and build bucket lists."""
+    lib = _lib.load()
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    N = int(nrows) * int(s)
+    if out is None:
+        out = BucketLists(m, s, nrows,
+                          torch.empty(m + 1, dtype=torch.int32, device=device),
+                          torch.empty(max(N, 1), dtype=torch.int32, device=device),
+                          torch.empty(max(N, 1), dtype=torch.int8, device=device))
+        if want_cols:
+            out.col_rows = torch.empty(max(N, 1), dtype=torch.int32, device=device)
+            out.col_signs = torch.empty(max(N, 1), dtype=torch.int8, device=device)
+        out.ws = _workspace(lib.skh_hash_workspace_bytes(nrows, m, s), device)
+    rc = lib.skh_hash_gen(int(seed) & (2**64 - 1), int(m), int(s), int(nrows), int(row0), int(blk), int(stride),
+                          _ptr(out.col_rows), _ptr(out.col_signs), _ptr(out.ptr), _ptr(out.rows), _ptr(out.signs),
+                          _ptr(out.ws), out.ws.numel(), _stream())
+    _lib.check(rc, "skh_hash_gen")
+    return out
+
+
+def hash_status(bl):
+    lib = _lib.load()
+    return lib.skh_hash_status(_ptr(bl.ws), _stream())
+
+
+def sketch_dense(bl, A, b=None, alpha=None, SA=None, Sb=None):
+    """R5 dense: SA = alpha * S A (alpha defaults to c_s), Sb likewise."""
+    lib = _lib.load()
+    _need_cuda(A, b)
+    if A.dtype != torch.float64:
+        raise ValueError("A must be float64")
+    n, d = A.shape
+    if SA is None:
+        SA = torch.empty(bl.m, d, dtype=torch.float64, device=A.device)
+    if b is not None and Sb is None:
+        Sb = torch.empty(bl.m, dtype=torch.float64, device=A.device)
+    alpha = c_s(bl.s) if alpha is None else float(alpha)
+    rc = lib.skh_sketch_dense(bl.m, bl.s, _ptr(bl.ptr), _ptr(bl.rows), _ptr(bl.signs), n, d, _ptr(A), _ld(A),
+                              _ptr(b), _ptr(SA), _ld(SA), _ptr(Sb), alpha, _stream())
+    _lib.check(rc, "skh_sketch_dense")
+    return SA, Sb
+
+
+def sketch_csr(bl, row_ptr, col_idx, val, d, b=None, alpha=None, SA=None, Sb=None):
+    """R5 sparse (CSR A): dense SA = alpha * S A."""
+    lib = _lib.load()
+    _need_cuda(row_ptr, col_idx, val, b)
+    n = row_ptr.numel() - 1
+    dev = row_ptr.device
+    if SA is None:
+        SA = torch.empty(bl.m, d, dtype=torch.float64, device=dev)
+    if b is not None and Sb is None:
+        Sb = torch.empty(bl.m, dtype=torch.float64, device=dev)
+    alpha = c_s(bl.s) if alpha is None else float(alpha)
+    rc = lib.skh_sketch_csr(bl.m, bl.s, _ptr(bl.ptr), _ptr(bl.rows), _ptr(bl.signs), n, int(d), _ptr(row_ptr),
+                            _ptr(col_idx), _ptr(val), _ptr(b), _ptr(SA), _ld(SA), _ptr(Sb), alpha, _stream())
+    _lib.check(rc, "skh_sketch_csr")
+    return SA, Sb
+
+
+def rht_stages(seed, X, bit_lo, bit_hi, nrows=None, row0=0, apply_diag=True, alpha=1.0, Y=None):
+    """R3+R4: Y = alpha * Hhat_[bit_lo,bit_hi) D? X along rows (X: nvalid x d)."""
+    lib = _lib.load()
+    _need_cuda(X)
+    nvalid, d = X.shape
+    nrows = nvalid if nrows is None else int(nrows)
+    if Y is None:
+        Y = torch.empty(nrows, d, dtype=torch.float64, device=X.device)
+    ws = _workspace(lib.skh_rht_stages_workspace_bytes(nvalid, row0), X.device) if apply_diag else None
+    rc = lib.skh_rht_stages(int(seed) & (2**64 - 1), nrows, nvalid, int(row0), d, _ptr(X), _ld(X), _ptr(Y), _ld(Y),
+                            int(bit_lo), int(bit_hi), int(bool(apply_diag)), float(alpha), _ptr(ws),
+                            0 if ws is None else ws.numel(), _stream())
+    _lib.check(rc, "skh_rht_stages")
+    return Y
+
+
+class RhtDense:
+    """Reusable workspace for skh_rht_dense (one allocation per shape)."""
+
+    def __init__(self, n, m, s, d, device=None):
+        lib = _lib.load()
+        self.n, self.m, self.s, self.d = int(n), int(m), int(s), int(d)
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        self.ws = _workspace(lib.skh_rht_dense_workspace_bytes(n, m, s, d), device)
+
+    def __call__(self, seed, A, b=None, SA=None, Sb=None):
+        lib = _lib.load()
+        _need_cuda(A, b)
+        if SA is None:
+            SA = torch.empty(self.m, self.d, dtype=torch.float64, device=A.device)
+        if b is not None and Sb is None:
+            Sb = torch.empty(self.m, dtype=torch.float64, device=A.device)
+        rc = lib.skh_rht_dense(int(seed) & (2**64 - 1), self.n, self.m, self.s, self.d, _ptr(A), _ld(A), _ptr(b),
+                               _ptr(SA), _ld(SA), _ptr(Sb), _ptr(self.ws), self.ws.numel(), _stream())
+        _lib.check(rc, "skh_rht_dense")
+        return SA, Sb
+
+    def from_host(self, seed, A_host, b_host=None, SA_host=None, Sb_host=None):
+        """Same from host (pinned) tensors; returns host SA, Sb after syncing the stream."""
+        lib = _lib.load()
+        if A_host.is_cuda:
+            raise ValueError("from_host takes CPU tensors")
+        if SA_host is None:
+            SA_host = torch.empty(self.m, self.d, dtype=torch.float64, pin_memory=True)
+        if b_host is not None and Sb_host is None:
+            Sb_host = torch.empty(self.m, dtype=torch.float64, pin_memory=True)
+        rc = lib.skh_rht_dense_host(int(seed) & (2**64 - 1), self.n, self.m, self.s, self.d, _ptr(A_host),
+                                    _ld(A_host), _ptr(b_host), _ptr(SA_host), _ld(SA_host), _ptr(Sb_host),
+                                    _ptr(self.ws), self.ws.numel(), _stream())
+        _lib.check(rc, "skh_rht_dense_host")
+        torch.cuda.current_stream().synchronize()
+        return SA_host, Sb_host
+
+
+def rht_dense(seed, A, b, m, s):
+    """R1-R5 on one GPU: SA = S_h H D A, Sb = S_h H D b (HRHT, L790-801)."""
+    n, d = A.shape
+    return RhtDense(n, m, s, d, A.device)(seed, A, b)
+
+
+class SketchDenseHost:
+    """Workspace + call for skh_sketch_dense_host (plain s-hashing from host buffers)."""
+
+    def __init__(self, n, m, s, d, device=None):
+        lib = _lib.load()
+        self.n, self.m, self.s, self.d = int(n), int(m), int(s), int(d)
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        self.ws = _workspace(lib.skh_sketch_dense_workspace_bytes(n, m, s, d), device)
+
+    def __call__(self, seed, A_host, b_host=None, SA_host=None, Sb_host=None):
+        lib = _lib.load()
+        if SA_host is None:
+            SA_host = torch.empty(self.m, self.d, dtype=torch.float64, pin_memory=True)
+        if b_host is not None and Sb_host is None:
+            Sb_host = torch.empty(self.m, dtype=torch.float64, pin_memory=True)
+        rc = lib.skh_sketch_dense_host(int(seed) & (2**64 - 1), self.n, self.m, self.s, self.d, _ptr(A_host),
+                                       _ld(A_host), _ptr(b_host), _ptr(SA_host), _ld(SA_host), _ptr(Sb_host),
+                                       _ptr(self.ws), self.ws.numel(), _stream())
+        _lib.check(rc, "skh_sketch_dense_host")
+        torch.cuda.current_stream().synchronize()
+        return SA_host, Sb_host
+
+
+def scale(X, alpha):
+    lib = _lib.load()
+    _need_cuda(X)
+    rows, cols = X.shape
+    _lib.check(lib.skh_scale(_ptr(X), rows, cols, _ld(X), float(alpha), _stream()), "skh_scale")
+    return X
+
+
+def ordered_sum(parts, alpha=1.0, out=None):
+    """parts: [G, rows, cols] contiguous; out = alpha * (((P0 + P1) + P2) + ...)."""
+    lib = _lib.load()
+    _need_cuda(parts)
+    G, rows, cols = parts.shape
+    if out is None:
+        out = torch.empty(rows, cols, dtype=torch.float64, device=parts.device)
+    rc = lib.skh_ordered_sum(_ptr(parts), G, parts.stride(0), rows, cols, parts.stride(1), _ptr(out), _ld(out),
+                             float(alpha), _stream())
+    _lib.check(rc, "skh_ordered_sum")
+    return out

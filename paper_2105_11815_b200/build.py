@@ -1,0 +1,70 @@
+"""Build the in-tree shared libraries with nvcc for sm_100a.
+
+  libskh.so   (paper_2105_11815_b200/csrc/*.cu)  -- the product: C ABI of include/skh.h
+  libsynth.so (synth/csrc/*.cu)                  -- device input generator (harness)
+
+Usage: python -m paper_2105_11815_b200.build [--force]
+"""
+import glob
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_2105_11815_b200")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+
+TARGETS = {
+    os.path.join(PKG, "libskh.so"): sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu"))),
+    os.path.join(ROOT, "synth", "libsynth.so"): sorted(glob.glob(os.path.join(ROOT, "synth", "csrc", "*.cu"))),
+}
+
+
+def _deps(srcs):
+    d = list(srcs)
+    for s in srcs:
+        d += glob.glob(os.path.join(os.path.dirname(s), "*.cuh"))
+    d += [os.path.join(ROOT, "include", "skh.h")]
+    return d
+
+
+def _stale(out, srcs):
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(s) > t for s in _deps(srcs) if os.path.exists(s))
+
+
+def build(force=False, verbose=False):
+    built = []
+    for out, srcs in TARGETS.items():
+        if not srcs:
+            continue
+        if not force and not _stale(out, srcs):
+            continue
+        objdir = os.path.join(os.path.dirname(out), "build_obj")
+        os.makedirs(objdir, exist_ok=True)
+        objs = []
+        for s in srcs:
+            o = os.path.join(objdir, os.path.basename(s).replace(".cu", ".o"))
+            cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed on {s}")
+            if verbose:
+                sys.stderr.write(r.stderr)
+            objs.append(o)
+        cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"link failed for {out}")
+        built.append(out)
+    return built
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,75 @@
+// common.cuh -- device helpers shared by the libskh kernels (product side).
+// Independent of oracle/: this is the CUDA implementation of the same
+// counter-based generator (R1), written from the definition.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/skh.h"
+
+namespace skh {
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kLabelHash = 0x48415348ull;  // "HASH"
+constexpr uint64_t kLabelDiag = 0x44494147ull;  // "DIAG"
+constexpr int kMaxAttempts = 0xFFFF;            // attempts t = 0..0xFFFE
+constexpr uint64_t kSignSlot = 0xFFFF;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+// Output number ctr+1 of splitmix64 started at state `key`.
+__host__ __device__ __forceinline__ uint64_t stream_u(uint64_t key, uint64_t ctr) {
+  return mix64(key + (ctr + 1) * kGamma);
+}
+
+__host__ __device__ __forceinline__ uint64_t key_hash(uint64_t seed) { return mix64(seed ^ kLabelHash); }
+__host__ __device__ __forceinline__ uint64_t key_diag(uint64_t seed) { return mix64(seed ^ kLabelDiag); }
+
+// Local column k -> global column of S (see skh_hash_gen).
+__host__ __device__ __forceinline__ int64_t row_map(int64_t k, int64_t row0, int64_t blk, int64_t stride) {
+  return blk <= 0 ? row0 + k : row0 + (k / blk) * stride + (k % blk);
+}
+
+// Thread-local error message (api.cu).
+void set_error(const char* fmt, ...);
+
+int check_launch(const char* what);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Kernel launchers (one per .cu file).
+// hash.cu
+size_t hash_ws_bytes(int64_t nrows, int64_t m, int s);
+int launch_hash(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, int64_t blk,
+                int64_t stride, int32_t* col_rows, int8_t* col_signs, int32_t* bucket_ptr,
+                int32_t* bucket_rows, int8_t* bucket_signs, void* ws, size_t ws_bytes,
+                cudaStream_t st);
+int hash_status(const void* ws, cudaStream_t st);
+// gather.cu
+int launch_gather_dense(int64_t m, const int32_t* ptr, const int32_t* rows, const int8_t* sg,
+                        int64_t d, const double* A, int64_t lda, double* SA, int64_t ldsa,
+                        double alpha, cudaStream_t st);
+int launch_gather_vec(int64_t m, const int32_t* ptr, const int32_t* rows, const int8_t* sg,
+                      const double* b, double* Sb, double alpha, cudaStream_t st);
+// csr.cu
+int launch_gather_csr(int64_t m, const int32_t* ptr, const int32_t* rows, const int8_t* sg,
+                      int64_t d, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
+                      double* SA, int64_t ldsa, double alpha, cudaStream_t st);
+// fwht.cu
+size_t fwht_ws_bytes(int64_t nrows, int64_t row0);
+int launch_fwht(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, int64_t d,
+                const double* X, int64_t ldx, double* Y, int64_t ldy, int bit_lo, int bit_hi,
+                int apply_diag, double alpha, void* ws, cudaStream_t st);
+// util (api.cu)
+int launch_scale(double* X, int64_t rows, int64_t cols, int64_t ldx, double alpha, cudaStream_t st);
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+}  // namespace skh

@@ -1,0 +1,155 @@
+// gather.cu -- R5 for dense X: SA[b, :] = alpha * (ascending-row signed sum of
+// X rows in bucket b)  (Alg. 1 Step 1; R10).
+//
+// Work unit: one warp = one bucket x one 64-column tile; each lane owns two
+// adjacent columns (one 16-byte load per row) and adds the bucket's rows
+// sequentially in list order, so every output is the oracle's exact sum.  No
+// atomics, no cross-lane reduction.  Rows are prefetched kU at a time (row ids
+// broadcast by shuffle) to keep 16*kU bytes per lane in flight.
+//
+// Scheduling: CTAs are ordered column-tile-major, so at any time
+// the grid works on one 64-column slice of X (n x 512 B); for s > 1 the s
+// reads of a row segment hit L2 instead of HBM as long as that slice fits in
+// L2 (C3: 131072 x 512 B = 64 MiB < 126 MB).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace skh {
+namespace {
+
+constexpr int kWarps = 8;       // buckets per CTA
+constexpr int kTileCols = 64;   // columns per warp
+constexpr int kU = 8;           // rows in flight per lane
+
+template <bool VEC2>
+__global__ void __launch_bounds__(kWarps * 32) gather_dense_kernel(
+    int64_t m, int64_t nbgroups, const int32_t* __restrict__ ptr, const int32_t* __restrict__ rows,
+    const int8_t* __restrict__ sg, int64_t d, const double* __restrict__ X, int64_t ldx,
+    double* __restrict__ SA, int64_t ldsa, double alpha) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t tile = blockIdx.x / nbgroups;
+  const int64_t b = (blockIdx.x % nbgroups) * kWarps + w;
+  if (b >= m) return;
+  const int64_t c0 = tile * kTileCols;
+  // VEC2: lane owns columns c0 + 2 lane, c0 + 2 lane + 1; else c0 + lane, c0 + 32 + lane.
+  const int64_t ca = VEC2 ? c0 + 2 * lane : c0 + lane;
+  const int64_t cb = VEC2 ? ca + 1 : c0 + 32 + lane;
+  const bool va = ca < d, vb = cb < d;
+  double acc0 = 0.0, acc1 = 0.0;
+  const int beg = ptr[b], end = ptr[b + 1];
+  for (int t0 = beg; t0 < end; t0 += 32) {
+    const int cnt = min(32, end - t0);
+    int my_row = 0, my_neg = 0;
+    if (lane < cnt) {
+      my_row = rows[t0 + lane];
+      my_neg = sg[t0 + lane] < 0;
+    }
+    for (int u0 = 0; u0 < cnt; u0 += kU) {
+      double x0[kU], x1[kU];
+      int ng[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int src = u0 + u;
+        const int r = __shfl_sync(0xffffffffu, my_row, src & 31);
+        ng[u] = __shfl_sync(0xffffffffu, my_neg, src & 31);
+        x0[u] = 0.0;
+        x1[u] = 0.0;
+        if (src < cnt) {
+          const double* p = X + (int64_t)r * ldx;
+          if (VEC2) {
+            if (vb) {
+              const double2 v = __ldg(reinterpret_cast<const double2*>(p + ca));
+              x0[u] = v.x;
+              x1[u] = v.y;
+            } else if (va) {
+              x0[u] = __ldg(p + ca);
+            }
+          } else {
+            if (va) x0[u] = __ldg(p + ca);
+            if (vb) x1[u] = __ldg(p + cb);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (u0 + u < cnt) {  // sequential, list order: the oracle's exact sum
+          acc0 = ng[u] ? acc0 - x0[u] : acc0 + x0[u];
+          acc1 = ng[u] ? acc1 - x1[u] : acc1 + x1[u];
+        }
+      }
+    }
+  }
+  double* o = SA + b * ldsa;
+  if (VEC2) {
+    if (vb) {
+      double2 v;
+      v.x = alpha * acc0;
+      v.y = alpha * acc1;
+      *reinterpret_cast<double2*>(o + ca) = v;
+    } else if (va) {
+      o[ca] = alpha * acc0;
+    }
+  } else {
+    if (va) o[ca] = alpha * acc0;
+    if (vb) o[cb] = alpha * acc1;
+  }
+}
+
+// Sb: one thread per bucket, sequential over its list with kU loads in flight.
+__global__ void gather_vec_kernel(int64_t m, const int32_t* __restrict__ ptr, const int32_t* __restrict__ rows,
+                                  const int8_t* __restrict__ sg, const double* __restrict__ x,
+                                  double* __restrict__ out, double alpha) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= m) return;
+  const int beg = ptr[b], end = ptr[b + 1];
+  double acc = 0.0;
+  for (int t0 = beg; t0 < end; t0 += kU) {
+    double v[kU];
+    int ng[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      v[u] = 0.0;
+      ng[u] = 0;
+      if (t0 + u < end) {
+        v[u] = __ldg(x + rows[t0 + u]);
+        ng[u] = sg[t0 + u] < 0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (t0 + u < end) acc = ng[u] ? acc - v[u] : acc + v[u];
+  }
+  out[b] = alpha * acc;
+}
+
+}  // namespace
+
+int launch_gather_dense(int64_t m, const int32_t* ptr, const int32_t* rows, const int8_t* sg, int64_t d,
+                        const double* X, int64_t ldx, double* SA, int64_t ldsa, double alpha, cudaStream_t st) {
+  const int64_t nbgroups = (m + kWarps - 1) / kWarps;
+  const int64_t ntiles = (d + kTileCols - 1) / kTileCols;
+  const int64_t grid = nbgroups * ntiles;
+  if (grid >= (1ll << 31)) {
+    set_error("gather grid too large");
+    return SKH_EOVERFLOW;
+  }
+  const bool vec2 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(SA)) % 16 == 0) &&
+                    (ldx % 2 == 0) && (ldsa % 2 == 0);
+  if (vec2)
+    gather_dense_kernel<true><<<(unsigned)grid, kWarps * 32, 0, st>>>(m, nbgroups, ptr, rows, sg, d, X, ldx, SA,
+                                                                       ldsa, alpha);
+  else
+    gather_dense_kernel<false><<<(unsigned)grid, kWarps * 32, 0, st>>>(m, nbgroups, ptr, rows, sg, d, X, ldx, SA,
+                                                                        ldsa, alpha);
+  return check_launch("gather_dense");
+}
+
+int launch_gather_vec(int64_t m, const int32_t* ptr, const int32_t* rows, const int8_t* sg, const double* b,
+                      double* Sb, double alpha, cudaStream_t st) {
+  gather_vec_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(m, ptr, rows, sg, b, Sb, alpha);
+  return check_launch("gather_vec");
+}
+
+}  // namespace skh
