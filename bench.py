@@ -1,0 +1,295 @@
+#!/usr/bin/env python
+"""Benchmark of the hashing-sketch hot path (BASELINE.json metric:
+"sketch GB/s of A streamed (S.A, S.H.D.A) & % HBM peak at 1/2/4/8 B200").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5] [--impl reference]
+
+A step is one pass of the whole hot path over the workload (SURVEY §8(a) rows
+R1-R5; R6/R7 as well when N > 1): hash_gen (draw S_h, bucket lists), the D +
+Walsh-Hadamard passes, the bucket gather producing SA and Sb.  Default workload
+C5 (BASELINE.json configs[4]: the config the metric is quoted on at 1/2/4/8
+GPUs; it fits one B200).  Inputs are synthetic (synth/), generated on the
+device and resident in HBM before timing; A (64 GiB) is larger than L2, so no
+flush is needed.  Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+# the CPU oracle is timed single-threaded ("cores": 1 in cpu_baseline)
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json: torch copy, read+write bytes)"
+    return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- CPU oracle (cpu_baseline / reference arm)
+def oracle_sample(cfg, ncols):
+    """Time the oracle as it stands on a bounded sample of the workload: ncols
+    columns of A (all n rows), or a row block for CSR.  Returns (bytes, seconds, what)."""
+    import numpy as np
+
+    from oracle import sketch
+    from synth import gen
+    if cfg.kind == "csr":
+        rows = max(1, int(cfg.n * ncols / 256))
+        sub = cfg.scaled(n=rows)
+        rp, ci, v = gen.csr(sub)
+        b = gen.rhs(sub)
+        t0 = time.perf_counter()
+        sketch.sketch_csr(cfg.seed, rp, ci, v, cfg.d, b, cfg.m, cfg.s)
+        t = time.perf_counter() - t0
+        return rows * cfg.nnz_row * 12 + (rows + 1) * 8, t, f"CSR rows 0..{rows} of {cfg.name} (all buckets)"
+    cols = list(range(ncols))
+    Ablk = gen.dense_block(cfg, 0, cfg.n, cols)
+    t0 = time.perf_counter()
+    if cfg.hd:
+        sketch.rht_sketch(cfg.seed, Ablk, None, cfg.m, cfg.s)
+    else:
+        sketch.sketch_dense(cfg.seed, Ablk, None, cfg.m, cfg.s)
+    t = time.perf_counter() - t0
+    del np
+    return cfg.n * ncols * 8, t, f"{ncols} of {cfg.d} columns of {cfg.name} A, all {cfg.n} rows"
+
+
+def cpu_baseline(cfg, target_s=12.0):
+    ncols = 1
+    nbytes, t, what = oracle_sample(cfg, ncols)
+    if t < target_s / 4 and cfg.kind != "csr":
+        ncols = max(1, min(cfg.d, int(ncols * target_s / max(t, 1e-3) / 2)))
+        nbytes, t, what = oracle_sample(cfg, ncols)
+    return {"value": nbytes / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{what}; {t:.2f} s single-threaded NumPy", "seconds": round(t, 3)}
+
+
+def reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    ncols = 2 if cfg.kind != "csr" else 4
+    for _ in range(args.warmup):
+        oracle_sample(cfg, ncols)
+    tot_b, tot_t = 0, 0.0
+    what = ""
+    for _ in range(args.steps):
+        nb, t, what = oracle_sample(cfg, ncols)
+        tot_b += nb
+        tot_t += t
+    v = tot_b / tot_t / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "n": cfg.n, "d": cfg.d, "m": cfg.m, "s": cfg.s, "hd": cfg.hd,
+                       "note": "CPU oracle on a bounded sample of the workload per step"},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{what} per step"},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "sketch GB/s of A streamed (S.A, S.H.D.A) & % HBM peak"
+
+
+# ---------------------------------------------------------------- GPU arm, one GPU
+def build_step(cfg, torch):
+    from paper_2105_11815_b200 import pipeline
+    from synth import device
+    if cfg.kind == "csr":
+        rp, ci, v = device.csr(cfg)
+        b = device.rhs(cfg)
+        return pipeline.CsrStep(cfg.seed, rp, ci, v, cfg.d, b, cfg.m, cfg.s, record=True), (rp, ci, v, b)
+    A = device.dense(cfg)
+    b = device.rhs(cfg)
+    cls = pipeline.HrhtStep if cfg.hd else pipeline.PlainStep
+    return cls(cfg.seed, A, b, cfg.m, cfg.s, record=True), (A, b)
+
+
+def e2e_measure(cfg, inputs, steps, torch):
+    """Same metric through the host-buffer C-ABI call: H2D of A and b and D2H of
+    SA and Sb inside the timed region (pinned host buffers)."""
+    import paper_2105_11815_b200 as skh
+    if cfg.kind == "csr":
+        return None
+    A, b = inputs
+    A_h = torch.empty(A.shape, dtype=torch.float64, pin_memory=True)
+    A_h.copy_(A)
+    b_h = torch.empty(b.shape, dtype=torch.float64, pin_memory=True)
+    b_h.copy_(b)
+    torch.cuda.synchronize()
+    if cfg.hd:
+        op = skh.RhtDense(cfg.n, cfg.m, cfg.s, cfg.d)
+        call = op.from_host
+    else:
+        op = skh.SketchDenseHost(cfg.n, cfg.m, cfg.s, cfg.d)
+        call = op
+    SA_h = torch.empty(cfg.m, cfg.d, dtype=torch.float64, pin_memory=True)
+    Sb_h = torch.empty(cfg.m, dtype=torch.float64, pin_memory=True)
+    call(cfg.seed, A_h, b_h, SA_h, Sb_h)  # warm-up
+    t = []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        call(cfg.seed, A_h, b_h, SA_h, Sb_h)
+        e1.record()
+        torch.cuda.synchronize()
+        t.append(e0.elapsed_time(e1))
+    del op
+    ms = sum(t) / len(t)
+    return {"value": cfg.a_bytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms, "steps": steps,
+            "h2d_bytes_per_step": A.numel() * 8 + b.numel() * 8, "d2h_bytes_per_step": cfg.m * cfg.d * 8 + cfg.m * 8,
+            "api": "skh_rht_dense_host" if cfg.hd else "skh_sketch_dense_host"}
+
+
+def roofline(cfg, step, stage_ms, peak_gbs, peak_src):
+    """Dominant kernel and its algorithmic bytes per launch."""
+    if cfg.kind == "csr":
+        name = "gather_csr"
+        nnz = cfg.n * cfg.nnz_row
+        alg = nnz * 12 + (cfg.n + 1) * 8 + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5
+        t = stage_ms[name]
+    elif cfg.hd:
+        passes = [k for k in stage_ms if k.startswith("fwht_pass")]
+        name = "fwht_fast (" + "+".join(str(k) for k in step.plan) + " stage passes, mean per launch)"
+        alg = 2 * step.n_pad * cfg.d * 8          # read + write the n x d block once per pass
+        t = sum(stage_ms[k] for k in passes) / len(passes)
+    else:
+        name = "gather_dense"
+        alg = cfg.n * cfg.d * 8 + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5
+        t = stage_ms["gather"]
+    achieved = alg / (t / 1e3) / 1e9
+    return {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
+            "frac": round(achieved / peak_gbs, 4), "traffic": None, "alg_bytes_per_launch": alg,
+            "ms_per_launch": round(t, 4), "peak_source": peak_src}
+
+
+def gpu_arm_single(args, cfg):
+    import torch
+
+    import paper_2105_11815_b200 as skh
+    torch.cuda.set_device(0)
+    step, inputs = build_step(cfg, torch)
+    torch.cuda.synchronize()
+    for _ in range(max(args.warmup, 0)):
+        step.run()
+    torch.cuda.synchronize()
+    timers = [step.new_timer() for _ in range(args.steps)]
+    clk = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0] or 0))
+    clk.start()
+    time.sleep(0.3)
+    n0 = skh.api.launch_count()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(args.steps):
+        step.run(timers[k])
+    e1.record()
+    torch.cuda.synchronize()
+    launches = skh.api.launch_count() - n0
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    per = [t.durations_ms() for t in timers]
+    stage_ms = {k: sum(p[k] for p in per) / len(per) for k in per[0]}
+    pk, src = peaks()
+    value = cfg.a_bytes / (ms / 1e3) / 1e9
+    line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "pct_hbm_peak": round(100 * value / pk["hbm_gbs"], 2),
+            "config": {"workload": cfg.name, "n": cfg.n, "d": cfg.d, "m": cfg.m, "s": cfg.s, "hd": cfg.hd,
+                       "a_bytes": cfg.a_bytes, "l2": "inputs (A) larger than L2; no flush",
+                       "parallelism": "single GPU", "note": cfg.note},
+            "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+            "gpu_launches": int(launches), "clocks": clocks}
+    line["roofline"] = roofline(cfg, step, stage_ms, pk["hbm_gbs"], src)
+    del step
+    if not args.no_e2e:
+        line["e2e"] = e2e_measure(cfg, inputs, args.e2e_steps, torch)
+    del inputs
+    torch.cuda.empty_cache()
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C5")
+    ap.add_argument("--impl", default="skh", choices=["skh", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from synth import configs
+    cfg = configs.ALL[args.workload]
+    if args.impl == "reference":
+        return reference_arm(args, cfg)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_2105_11815_b200 import sharded_bench
+        return sharded_bench.run(args, cfg)
+    from paper_2105_11815_b200 import build
+    build.build()
+    return gpu_arm_single(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

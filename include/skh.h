@@ -64,6 +64,9 @@ const char* skh_strerror(int code);
 const char* skh_last_error(void);
 /* ABI version, currently 1. */
 int skh_abi_version(void);
+/* Number of CUDA kernels this process has enqueued through libskh so far
+ * (monotonic, all threads and devices); lets a caller count its launches. */
+uint64_t skh_launch_count(void);
 
 /* ------------------------------------------------------------------------ *
  * Scale constants (R5, R9, R10).  Each is one IEEE sqrt followed by
@@ -163,6 +166,12 @@ int skh_sketch_csr(int64_t m, int32_t s,
  *   bytes (may be NULL when apply_diag == 0).
  * ------------------------------------------------------------------------ */
 size_t skh_rht_stages_workspace_bytes(int64_t nvalid, int64_t row0);
+/* The HBM-pass split skh_rht_stages uses for `nbits` stages on rows of length d
+ * (aligned != 0: X, Y 16-byte aligned with even leading dimensions).  Writes
+ * the stage count of each pass (low bits first) into bits_out[0..] and returns
+ * the number of passes (at most max_out are written).  One skh_rht_stages call
+ * per returned range launches exactly one transform kernel. */
+int skh_rht_pass_plan(int nbits, int64_t d, int aligned, int* bits_out, int max_out);
 int skh_rht_stages(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0,
                    int64_t d, const double* X, int64_t ldx, double* Y, int64_t ldy,
                    int bit_lo, int bit_hi, int apply_diag, double alpha,

@@ -17,6 +17,7 @@ SIGNATURES = {
     "skh_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "skh_last_error": (ctypes.c_char_p, []),
     "skh_abi_version": (ctypes.c_int, []),
+    "skh_launch_count": (c_u64, []),
     "skh_c_s": (c_d, [c_i32]),
     "skh_c_n": (c_d, [c_i64]),
     "skh_c_ns": (c_d, [c_i64, c_i32]),
@@ -29,6 +30,8 @@ SIGNATURES = {
     "skh_sketch_csr": (ctypes.c_int, [c_i64, c_i32, c_p, c_p, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p,
                                       c_d, c_p]),
     "skh_rht_stages_workspace_bytes": (c_sz, [c_i64, c_i64]),
+    "skh_rht_pass_plan": (ctypes.c_int, [ctypes.c_int, c_i64, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                         ctypes.c_int]),
     "skh_rht_stages": (ctypes.c_int, [c_u64, c_i64, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_i64, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_int, c_d, c_p, c_sz, c_p]),
     "skh_rht_dense_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32, c_i64]),

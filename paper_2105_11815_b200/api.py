@@ -128,15 +128,40 @@ def sketch_csr(bl, row_ptr, col_idx, val, d, b=None, alpha=None, SA=None, Sb=Non
     return SA, Sb
 
 
-def rht_stages(seed, X, bit_lo, bit_hi, nrows=None, row0=0, apply_diag=True, alpha=1.0, Y=None):
+def launch_count():
+    """Kernels enqueued through libskh by this process so far."""
+    return int(_lib.load().skh_launch_count())
+
+
+def rht_pass_plan(nbits, d, aligned=True):
+    """Stage counts of the HBM passes skh_rht_stages uses (low bits first)."""
+    import ctypes
+    lib = _lib.load()
+    buf = (ctypes.c_int * 64)()
+    k = lib.skh_rht_pass_plan(int(nbits), int(d), int(bool(aligned)), buf, 64)
+    return [buf[i] for i in range(k)]
+
+
+def rht_stages_workspace(nvalid, row0=0, device=None):
+    lib = _lib.load()
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    return _workspace(lib.skh_rht_stages_workspace_bytes(int(nvalid), int(row0)), device)
+
+
+def rht_stages(seed, X, bit_lo, bit_hi, nrows=None, row0=0, apply_diag=True, alpha=1.0, Y=None, ws=None):
     """R3+R4: Y = alpha * Hhat_[bit_lo,bit_hi) D? X along rows (X: nvalid x d)."""
     lib = _lib.load()
     _need_cuda(X)
+    if X.dim() == 1:
+        X = X.view(-1, 1)
+        if Y is not None:
+            Y = Y.view(-1, 1)
     nvalid, d = X.shape
     nrows = nvalid if nrows is None else int(nrows)
     if Y is None:
         Y = torch.empty(nrows, d, dtype=torch.float64, device=X.device)
-    ws = _workspace(lib.skh_rht_stages_workspace_bytes(nvalid, row0), X.device) if apply_diag else None
+    if apply_diag and ws is None:
+        ws = rht_stages_workspace(nvalid, row0, X.device)
     rc = lib.skh_rht_stages(int(seed) & (2**64 - 1), nrows, nvalid, int(row0), d, _ptr(X), _ld(X), _ptr(Y), _ld(Y),
                             int(bit_lo), int(bit_hi), int(bool(apply_diag)), float(alpha), _ptr(ws),
                             0 if ws is None else ws.numel(), _stream())

@@ -8,6 +8,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -23,6 +24,9 @@ void set_error(const char* fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
 }
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -221,6 +225,7 @@ const char* skh_strerror(int code) {
 
 const char* skh_last_error(void) { return g_err; }
 int skh_abi_version(void) { return 1; }
+uint64_t skh_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 double skh_c_s(int32_t s) { return 1.0 / sqrt((double)s); }
 double skh_c_n(int64_t n_pad) { return 1.0 / sqrt((double)n_pad); }
@@ -305,6 +310,14 @@ int skh_sketch_csr(int64_t m, int32_t s, const int32_t* bucket_ptr, const int32_
 size_t skh_rht_stages_workspace_bytes(int64_t nvalid, int64_t row0) {
   if (nvalid < 0 || row0 < 0) return 0;
   return fwht_ws_bytes(nvalid, row0);
+}
+
+int skh_rht_pass_plan(int nbits, int64_t d, int aligned, int* bits_out, int max_out) {
+  if (nbits < 0 || d < 1) return 0;
+  const bool fast = aligned && d % 2 == 0 && d >= 16;
+  std::vector<int> ks = plan_passes(nbits, fast);
+  for (int i = 0; i < (int)ks.size() && i < max_out; ++i) bits_out[i] = ks[i];
+  return (int)ks.size();
 }
 
 int skh_rht_stages(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, int64_t d, const double* X,
@@ -509,7 +522,7 @@ int skh_scale(double* X, int64_t rows, int64_t cols, int64_t ldx, double alpha, 
   }
   const int64_t N = rows * cols;
   if (N == 0) return SKH_OK;
-  scale_kernel<<<(unsigned)((N + 255) / 256), 256, 0, as_stream(stream)>>>(X, rows, cols, ldx, alpha);
+  scale_kernel<<<(unsigned)((N + 255) / 256), 256, 0, as_stream(stream)>>>(X, rows, cols, ldx, alpha); note_launch();
   return check_launch("scale");
 }
 
@@ -522,7 +535,7 @@ int skh_ordered_sum(const double* parts, int64_t G, int64_t part_stride, int64_t
   const int64_t N = rows * cols;
   if (N == 0) return SKH_OK;
   ordered_sum_kernel<<<(unsigned)((N + 255) / 256), 256, 0, as_stream(stream)>>>(parts, G, part_stride, rows, cols,
-                                                                                  ldp, out, ldo, alpha);
+                                                                                  ldp, out, ldo, alpha); note_launch();
   return check_launch("ordered_sum");
 }
 

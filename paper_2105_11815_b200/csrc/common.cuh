@@ -42,6 +42,9 @@ void set_error(const char* fmt, ...);
 
 int check_launch(const char* what);
 
+// Process-wide count of kernels enqueued by libskh (skh_launch_count()).
+void note_launch();
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Kernel launchers (one per .cu file).

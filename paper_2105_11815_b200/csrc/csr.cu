@@ -120,13 +120,9 @@ int launch_gather_csr(int64_t m, const int32_t* ptr, const int32_t* rows, const 
     return SKH_EOVERFLOW;
   }
   const size_t smem = sizeof(double) * (size_t)tile;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gather_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxTile * 8);
-    attr_set = true;
-  }
+  cudaFuncSetAttribute(gather_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxTile * 8);
   gather_csr_kernel<<<(unsigned)grid, kThreads, smem, st>>>(m, ntiles, tile, ptr, rows, sg, d, row_ptr, col_idx,
-                                                              val, SA, ldsa, alpha);
+                                                              val, SA, ldsa, alpha); note_launch();
   return check_launch("gather_csr");
 }
 

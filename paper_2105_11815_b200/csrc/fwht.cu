@@ -179,7 +179,7 @@ int launch_fast(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nr
   for (int64_t g0 = g_begin; g0 < g_begin + g_count; g0 += max_groups) {
     const int64_t gc = min(max_groups, g_begin + g_count - g0);
     fwht_fast_kernel<K><<<(unsigned)(gc * ntc), kThreads, smem, st>>>(X, ldx, Y, ldy, nvalid, lo, d, ntc, g0, dw,
-                                                                      row0, w0, apply_diag, alpha);
+                                                                      row0, w0, apply_diag, alpha); note_launch();
   }
   return check_launch("fwht_fast");
 }
@@ -194,7 +194,7 @@ int launch_generic(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t
     const int64_t gc = min(step, g_begin + g_count - g0);
     const int64_t threads = gc * d;
     fwht_generic_kernel<K><<<(unsigned)((threads + kThreads - 1) / kThreads), kThreads, 0, st>>>(
-        X, ldx, Y, ldy, nvalid, lo, d, g0, gc, dw, row0, w0, apply_diag, alpha);
+        X, ldx, Y, ldy, nvalid, lo, d, g0, gc, dw, row0, w0, apply_diag, alpha); note_launch();
   }
   return check_launch("fwht_generic");
 }
@@ -256,7 +256,7 @@ size_t fwht_ws_bytes(int64_t nvalid, int64_t row0) {
 int launch_diag_words(uint64_t seed, int64_t nvalid, int64_t row0, void* ws, cudaStream_t st) {
   if (nvalid <= 0) return SKH_OK;
   const int64_t w0 = row0 >> 6, nw = ((row0 + nvalid - 1) >> 6) - w0 + 1;
-  diag_words_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(key_diag(seed), w0, nw, (uint64_t*)ws);
+  diag_words_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(key_diag(seed), w0, nw, (uint64_t*)ws); note_launch();
   return check_launch("diag_words");
 }
 

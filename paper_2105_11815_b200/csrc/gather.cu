@@ -143,12 +143,13 @@ int launch_gather_dense(int64_t m, const int32_t* ptr, const int32_t* rows, cons
   else
     gather_dense_kernel<false><<<(unsigned)grid, kWarps * 32, 0, st>>>(m, nbgroups, ptr, rows, sg, d, X, ldx, SA,
                                                                         ldsa, alpha);
+  note_launch();
   return check_launch("gather_dense");
 }
 
 int launch_gather_vec(int64_t m, const int32_t* ptr, const int32_t* rows, const int8_t* sg, const double* b,
                       double* Sb, double alpha, cudaStream_t st) {
-  gather_vec_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(m, ptr, rows, sg, b, Sb, alpha);
+  gather_vec_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(m, ptr, rows, sg, b, Sb, alpha); note_launch();
   return check_launch("gather_vec");
 }
 

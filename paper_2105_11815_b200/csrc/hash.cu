@@ -185,9 +185,9 @@ __global__ void scan_apply_kernel(int32_t* __restrict__ a, int64_t len, const in
 int excl_scan(int32_t* a, int64_t len, int32_t* bs, cudaStream_t st) {
   const int64_t nb = scan_blocks(len);
   if (nb == 0) return SKH_OK;
-  scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(a, len, bs);
-  scan_single_kernel<<<1, kScanThreads, 0, st>>>(bs, nb);
-  scan_apply_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(a, len, bs);
+  scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(a, len, bs); note_launch();
+  scan_single_kernel<<<1, kScanThreads, 0, st>>>(bs, nb); note_launch();
+  scan_apply_kernel<<<(unsigned)nb, kScanThreads, 0, st>>>(a, len, bs); note_launch();
   return check_launch("scan");
 }
 
@@ -296,7 +296,7 @@ int launch_hash(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, in
   (void)ws_bytes;
   cudaMemsetAsync(w.status, 0, sizeof(int32_t), st);
   if (N == 0) {
-    fill_i32_kernel<<<(unsigned)((m + 1 + 255) / 256), 256, 0, st>>>(bucket_ptr, m + 1, 0);
+    fill_i32_kernel<<<(unsigned)((m + 1 + 255) / 256), 256, 0, st>>>(bucket_ptr, m + 1, 0); note_launch();
     return check_launch("hash(empty)");
   }
   const uint64_t key = key_hash(seed);
@@ -308,6 +308,7 @@ int launch_hash(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, in
   else if (s <= 4) SKH_HASH_LAUNCH(4);
   else if (s <= 8) SKH_HASH_LAUNCH(8);
   else SKH_HASH_LAUNCH(64);
+  note_launch();
 #undef SKH_HASH_LAUNCH
   int rc = check_launch("hash_kernel");
   if (rc) return rc;
@@ -319,17 +320,17 @@ int launch_hash(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, in
   uint64_t* dst = w.keys_b;
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
-    upsweep_kernel<<<(unsigned)w.ntiles, kSortThreads, 0, st>>>(src, N, shift, w.hist, w.ntiles);
+    upsweep_kernel<<<(unsigned)w.ntiles, kSortThreads, 0, st>>>(src, N, shift, w.hist, w.ntiles); note_launch();
     rc = excl_scan(w.hist, 256 * w.ntiles, w.blocksums, st);
     if (rc) return rc;
-    downsweep_kernel<<<(unsigned)w.ntiles, kSortThreads, 0, st>>>(src, dst, N, shift, w.hist, w.ntiles);
+    downsweep_kernel<<<(unsigned)w.ntiles, kSortThreads, 0, st>>>(src, dst, N, shift, w.hist, w.ntiles); note_launch();
     rc = check_launch("radix pass");
     if (rc) return rc;
     uint64_t* t = src;
     src = dst;
     dst = t;
   }
-  finalize_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(src, N, m, bucket_ptr, bucket_rows, bucket_signs);
+  finalize_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(src, N, m, bucket_ptr, bucket_rows, bucket_signs); note_launch();
   return check_launch("finalize");
 }
 

@@ -1,0 +1,148 @@
+"""One step of the hot path (all SURVEY §8(a) rows) with preallocated buffers,
+composed from the C-ABI calls so each kernel can be timed live with CUDA
+events on the launching stream.  bench.py times these steps and the full-size
+parity tests run the same launch configuration.
+
+  HrhtStep  : R1+R2 hash_gen, R3+R4 rht_stages (one call per HBM pass, D fused
+              into the first), R5 sketch_dense with alpha = c_ns (C2, C3HD, C5)
+  PlainStep : R1+R2, R5 sketch_dense with alpha = c_s (C1, C3)
+  CsrStep   : R1+R2, R5 sketch_csr (C4)
+"""
+import torch
+
+from . import api
+
+
+def _ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+class _Timed:
+    """Records an event after each named stage (stage timing inside the timed region)."""
+
+    def __init__(self, names, record):
+        self.names = list(names)
+        self.record = record
+        self.events = [_ev() for _ in range(len(self.names) + 1)] if record else None
+        self.i = 0
+
+    def start(self):
+        if self.record:
+            self.events[0].record()
+        self.i = 0
+
+    def mark(self):
+        self.i += 1
+        if self.record:
+            self.events[self.i].record()
+
+    def durations_ms(self):
+        """Per-stage durations (call after synchronize)."""
+        return {n: self.events[k].elapsed_time(self.events[k + 1]) for k, n in enumerate(self.names)}
+
+
+class HrhtStep:
+    """SA = S_h H D A, Sb = S_h H D b for a row-major A resident on the device."""
+
+    def __init__(self, seed, A, b, m, s, record=False):
+        self.seed, self.m, self.s = seed, int(m), int(s)
+        self.A, self.b = A, b
+        n, d = A.shape
+        self.n, self.d = n, d
+        n_pad = 1
+        while n_pad < n:
+            n_pad *= 2
+        self.n_pad = n_pad
+        self.L = n_pad.bit_length() - 1
+        aligned = A.data_ptr() % 16 == 0 and A.stride(0) % 2 == 0
+        self.plan = api.rht_pass_plan(self.L, d, aligned)
+        dev = A.device
+        self.Y = torch.empty(n_pad, d, dtype=torch.float64, device=dev)
+        self.yb = torch.empty(n_pad, 1, dtype=torch.float64, device=dev) if b is not None else None
+        self.SA = torch.empty(self.m, d, dtype=torch.float64, device=dev)
+        self.Sb = torch.empty(self.m, dtype=torch.float64, device=dev) if b is not None else None
+        self.bl = None
+        self.ws = api.rht_stages_workspace(n, 0, dev)
+        self.alpha = api.c_ns(n_pad, s)
+        names = ["hash_gen"] + [f"fwht_pass{p}" for p in range(len(self.plan))]
+        if b is not None:
+            names.append("fwht_b")
+        names.append("gather")
+        self.timer = _Timed(names, record)
+
+    def new_timer(self):
+        return _Timed(self.timer.names, True)
+
+    def run(self, timer=None):
+        t = timer or self.timer
+        t.start()
+        self.bl = api.hash_gen(self.seed, self.m, self.s, self.n_pad, out=self.bl)
+        t.mark()
+        lo = 0
+        for p, k in enumerate(self.plan):
+            src = self.A if p == 0 else self.Y
+            api.rht_stages(self.seed, src, lo, lo + k, nrows=self.n_pad, apply_diag=(p == 0), alpha=1.0, Y=self.Y,
+                           ws=self.ws)
+            lo += k
+            t.mark()
+        if self.b is not None:
+            api.rht_stages(self.seed, self.b.view(-1, 1), 0, self.L, nrows=self.n_pad, apply_diag=True, alpha=1.0,
+                           Y=self.yb, ws=self.ws)
+            t.mark()
+        api.sketch_dense(self.bl, self.Y, None if self.b is None else self.yb.view(-1), alpha=self.alpha, SA=self.SA,
+                         Sb=self.Sb)
+        t.mark()
+        return self.SA, self.Sb
+
+
+class PlainStep:
+    """SA = S A, Sb = S b (s-hashing, no transform)."""
+
+    def __init__(self, seed, A, b, m, s, record=False):
+        self.seed, self.m, self.s = seed, int(m), int(s)
+        self.A, self.b = A, b
+        n, d = A.shape
+        dev = A.device
+        self.SA = torch.empty(self.m, d, dtype=torch.float64, device=dev)
+        self.Sb = torch.empty(self.m, dtype=torch.float64, device=dev) if b is not None else None
+        self.bl = None
+        self.timer = _Timed(["hash_gen", "gather"], record)
+
+    def new_timer(self):
+        return _Timed(self.timer.names, True)
+
+    def run(self, timer=None):
+        t = timer or self.timer
+        t.start()
+        self.bl = api.hash_gen(self.seed, self.m, self.s, self.A.shape[0], out=self.bl)
+        t.mark()
+        api.sketch_dense(self.bl, self.A, self.b, SA=self.SA, Sb=self.Sb)
+        t.mark()
+        return self.SA, self.Sb
+
+
+class CsrStep:
+    """Dense SA = S A, Sb = S b for CSR A."""
+
+    def __init__(self, seed, row_ptr, col_idx, val, d, b, m, s, record=False):
+        self.seed, self.m, self.s, self.d = seed, int(m), int(s), int(d)
+        self.csr = (row_ptr, col_idx, val)
+        self.b = b
+        dev = row_ptr.device
+        self.SA = torch.empty(self.m, self.d, dtype=torch.float64, device=dev)
+        self.Sb = torch.empty(self.m, dtype=torch.float64, device=dev) if b is not None else None
+        self.bl = None
+        self.timer = _Timed(["hash_gen", "gather_csr"], record)
+
+    def new_timer(self):
+        return _Timed(self.timer.names, True)
+
+    def run(self, timer=None):
+        t = timer or self.timer
+        t.start()
+        n = self.csr[0].numel() - 1
+        self.bl = api.hash_gen(self.seed, self.m, self.s, n, out=self.bl)
+        t.mark()
+        api.sketch_csr(self.bl, *self.csr, self.d, self.b, SA=self.SA, Sb=self.Sb)
+        t.mark()
+        return self.SA, self.Sb

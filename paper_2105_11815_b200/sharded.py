@@ -1,0 +1,207 @@
+"""Multi-GPU sequencing of the hot path.
+
+One process per GPU; torch.distributed (NCCL over NVLink/NVSwitch) carries the
+two exchange steps the method has when A is row-sharded:
+
+  R7  butterfly exchange (H D A only): H_n = H_G (x) H_{n/G} in the Sylvester
+      (natural) order of P:L796, so after the local stages on the low
+      log2(n/G) bits of the row index, ONE all-to-all that swaps the rank bits
+      with the top log2(G) local bits makes the remaining stages local.
+  R6  reduction of the m x d partial sketches: SA = sum_g S_g A_g (linearity of
+      Alg. 1 Step 1).  Deterministic (M5): an all-to-all of row strips
+      followed by a fixed rank-order sum in our kernel (skh_ordered_sum), so the
+      result does not depend on NCCL's reduction order.
+
+The per-rank compute goes through an ``ops`` object.  ``CudaOps`` (the
+product) calls libskh; the CPU tests pass an oracle-backed implementation to
+check this module's index algebra with the gloo backend.  There is no CPU
+fallback in the product path.
+"""
+import math
+
+import torch
+import torch.distributed as dist
+
+
+class CudaOps:
+    """libskh behind the ops interface (device tensors, current stream)."""
+
+    def __init__(self):
+        from . import api
+        self.api = api
+
+    def hash_gen(self, seed, m, s, nrows, row0, blk, stride, out=None):
+        return self.api.hash_gen(seed, m, s, nrows, row0=row0, blk=blk, stride=stride, out=out)
+
+    def rht_stages(self, seed, X, bit_lo, bit_hi, nrows, row0, apply_diag, Y, ws=None):
+        return self.api.rht_stages(seed, X, bit_lo, bit_hi, nrows=nrows, row0=row0, apply_diag=apply_diag,
+                                   alpha=1.0, Y=Y, ws=ws)
+
+    def sketch_dense(self, bl, X, b, alpha, SA=None, Sb=None):
+        return self.api.sketch_dense(bl, X, b, alpha=alpha, SA=SA, Sb=Sb)
+
+    def ordered_sum(self, parts, alpha, out=None):
+        return self.api.ordered_sum(parts, alpha=alpha, out=out)
+
+    def c_ns(self, n_pad, s):
+        return self.api.c_ns(n_pad, s)
+
+    def c_s(self, s):
+        return self.api.c_s(s)
+
+
+def _log2(x):
+    k = int(x).bit_length() - 1
+    if (1 << k) != x:
+        raise ValueError(f"{x} is not a power of two")
+    return k
+
+
+def strip_rows(m, G):
+    """Row strips of the reduce step: rank r owns rows [r*mq, min(m, (r+1)*mq))."""
+    mq = (m + G - 1) // G
+    return mq, [(r * mq, min(m, (r + 1) * mq)) for r in range(G)]
+
+
+class ShardedHrht:
+    """SA = S_h H D A over G ranks holding contiguous row blocks of A (n = 2^k,
+    G = 2^g <= n).  run() returns this rank's strip (rows lo:hi of SA) and of Sb."""
+
+    def __init__(self, seed, A_loc, b_loc, n, m, s, ops=None, group=None):
+        self.ops = ops or CudaOps()
+        self.group = group
+        self.G = dist.get_world_size(group)
+        self.r = dist.get_rank(group)
+        self.seed, self.n, self.m, self.s = seed, int(n), int(m), int(s)
+        self.L = self.n // self.G
+        if self.L * self.G != self.n or A_loc.shape[0] != self.L:
+            raise ValueError("A_loc must hold n / G rows")
+        _log2(self.n)
+        self.lg = _log2(self.L)
+        self.lq = _log2(self.L // self.G) if self.L >= self.G else None
+        if self.lq is None:
+            raise ValueError("need n / G >= G")
+        self.A, self.b = A_loc, b_loc
+        d = A_loc.shape[1]
+        self.d = d
+        kw = dict(dtype=A_loc.dtype, device=A_loc.device)
+        self.Y = torch.empty(self.L, d, **kw)
+        self.Y2 = torch.empty(self.L, d, **kw)
+        self.yb = torch.empty(self.L, 1, **kw) if b_loc is not None else None
+        self.yb2 = torch.empty(self.L, 1, **kw) if b_loc is not None else None
+        self.mq, self.strips = strip_rows(self.m, self.G)
+        self.P = torch.zeros(self.G * self.mq, d, **kw)      # partial, padded to G strips
+        self.Pb = torch.zeros(self.G * self.mq, **kw) if b_loc is not None else None
+        self.R = torch.empty(self.G, self.mq, d, **kw)       # received strips
+        self.Rb = torch.empty(self.G, self.mq, **kw) if b_loc is not None else None
+        self.out = torch.empty(self.mq, d, **kw)
+        self.outb = torch.empty(self.mq, 1, **kw) if b_loc is not None else None
+        self.bl = None
+        self.alpha = self.ops.c_ns(self.n, self.s)
+        self.ws = None
+        if isinstance(self.ops, CudaOps):
+            self.ws = self.ops.api.rht_stages_workspace(self.L, self.r * self.L, A_loc.device)
+
+    def run(self):
+        ops, G, r, L = self.ops, self.G, self.r, self.L
+        blk = L // G
+        # R3 + R4 (local): global bits [0, log2 L) = local bits, D with global ids
+        ops.rht_stages(self.seed, self.A, 0, self.lg, L, r * L, True, self.Y, self.ws)
+        if self.b is not None:
+            ops.rht_stages(self.seed, self.b.view(-1, 1), 0, self.lg, L, r * L, True, self.yb, self.ws)
+        # R7: block q of rows [q*blk, (q+1)*blk) -> rank q (equal splits)
+        if G > 1:
+            dist.all_to_all_single(self.Y2, self.Y, group=self.group)
+            if self.b is not None:
+                dist.all_to_all_single(self.yb2, self.yb, group=self.group)
+        else:
+            self.Y2.copy_(self.Y)
+            if self.b is not None:
+                self.yb2.copy_(self.yb)
+        # Y2 row k = g*blk + t holds global row g*L + r*blk + t; the rank bits g are
+        # local bits [log2 blk, log2 L): the remaining global stages, low to high.
+        ops.rht_stages(self.seed, self.Y2, self.lq, self.lg, L, 0, False, self.Y2, self.ws)
+        if self.b is not None:
+            ops.rht_stages(self.seed, self.yb2, self.lq, self.lg, L, 0, False, self.yb2, self.ws)
+        # R1 + R2 for exactly these global rows (ascending in k)
+        self.bl = ops.hash_gen(self.seed, self.m, self.s, L, r * blk, blk, L, out=self.bl)
+        # R5: unscaled partial sums of this rank's rows
+        ops.sketch_dense(self.bl, self.Y2, None if self.b is None else self.yb2.view(-1), 1.0,
+                         SA=self.P[: self.m], Sb=None if self.b is None else self.Pb[: self.m])
+        # R6 (M5): strips to their owners, then a rank-order sum scaled once by c_ns
+        lo, hi = self.strips[r]
+        if G > 1:
+            dist.all_to_all_single(self.R.view(G * self.mq, self.d), self.P, group=self.group)
+            if self.b is not None:
+                dist.all_to_all_single(self.Rb.view(-1), self.Pb, group=self.group)
+        else:
+            self.R[0].copy_(self.P)
+            if self.b is not None:
+                self.Rb[0].copy_(self.Pb)
+        ops.ordered_sum(self.R, self.alpha, out=self.out)
+        Sb = None
+        if self.b is not None:
+            ops.ordered_sum(self.Rb.view(G, self.mq, 1), self.alpha, out=self.outb)
+            Sb = self.outb[: hi - lo, 0]
+        return self.out[: hi - lo], Sb, (lo, hi)
+
+
+class ShardedPlain:
+    """SA = S A (s-hashing, no transform) over G ranks with contiguous row blocks."""
+
+    def __init__(self, seed, A_loc, b_loc, n, m, s, ops=None, group=None):
+        self.ops = ops or CudaOps()
+        self.group = group
+        self.G = dist.get_world_size(group)
+        self.r = dist.get_rank(group)
+        self.seed, self.n, self.m, self.s = seed, int(n), int(m), int(s)
+        per = (self.n + self.G - 1) // self.G
+        self.row0 = min(self.n, self.r * per)
+        self.nloc = min(self.n, self.row0 + per) - self.row0
+        if A_loc.shape[0] != self.nloc:
+            raise ValueError(f"rank {self.r} must hold rows [{self.row0}, {self.row0 + self.nloc})")
+        self.A, self.b = A_loc, b_loc
+        d = A_loc.shape[1]
+        self.d = d
+        kw = dict(dtype=A_loc.dtype, device=A_loc.device)
+        self.mq, self.strips = strip_rows(self.m, self.G)
+        self.P = torch.zeros(self.G * self.mq, d, **kw)
+        self.Pb = torch.zeros(self.G * self.mq, **kw) if b_loc is not None else None
+        self.R = torch.empty(self.G, self.mq, d, **kw)
+        self.Rb = torch.empty(self.G, self.mq, **kw) if b_loc is not None else None
+        self.out = torch.empty(self.mq, d, **kw)
+        self.outb = torch.empty(self.mq, 1, **kw) if b_loc is not None else None
+        self.bl = None
+        self.alpha = self.ops.c_s(self.s)
+
+    def run(self):
+        ops, G, r = self.ops, self.G, self.r
+        self.bl = ops.hash_gen(self.seed, self.m, self.s, self.nloc, self.row0, 0, 0, out=self.bl)
+        ops.sketch_dense(self.bl, self.A, self.b, 1.0, SA=self.P[: self.m],
+                         Sb=None if self.b is None else self.Pb[: self.m])
+        lo, hi = self.strips[r]
+        if G > 1:
+            dist.all_to_all_single(self.R.view(G * self.mq, self.d), self.P, group=self.group)
+            if self.b is not None:
+                dist.all_to_all_single(self.Rb.view(-1), self.Pb, group=self.group)
+        else:
+            self.R[0].copy_(self.P)
+            if self.b is not None:
+                self.Rb[0].copy_(self.Pb)
+        ops.ordered_sum(self.R, self.alpha, out=self.out)
+        Sb = None
+        if self.b is not None:
+            ops.ordered_sum(self.Rb.view(G, self.mq, 1), self.alpha, out=self.outb)
+            Sb = self.outb[: hi - lo, 0]
+        return self.out[: hi - lo], Sb, (lo, hi)
+
+
+def gather_strips(strip, lohi, m, group=None):
+    """Collect every rank's strip on all ranks (test / user convenience)."""
+    G = dist.get_world_size(group)
+    mq = math.ceil(m / G)
+    buf = torch.zeros(mq, *strip.shape[1:], dtype=strip.dtype, device=strip.device)
+    buf[: strip.shape[0]] = strip
+    allb = [torch.empty_like(buf) for _ in range(G)]
+    dist.all_gather(allb, buf, group=group)
+    return torch.cat(allb, 0)[:m]

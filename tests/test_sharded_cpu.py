@@ -1,0 +1,125 @@
+"""The multi-GPU sequencing (paper_2105_11815_b200/sharded.py) on CPU with the
+gloo backend, world sizes 2 and 4.  The per-rank compute is the oracle (an
+ops object defined here, in tests/), so these tests check the index algebra
+of the butterfly all-to-all (R7), the row maps handed to hash_gen, and the
+deterministic strip reduction (R6) against the unsharded oracle:
+  * real inputs: relative Frobenius error <= 1e-12 (BASELINE.json);
+  * integer inputs: bit-identical (every partial sum is an exact integer).
+"""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import hadamard, hashing, sketch
+from synth import gen
+
+
+class OracleOps:
+    """The oracle behind sharded.py's ops interface (CPU tensors)."""
+
+    class BL:
+        def __init__(self, m, s, ptr, rows, signs):
+            self.m, self.s, self.ptr, self.rows, self.signs = m, s, ptr, rows, signs
+
+    def hash_gen(self, seed, m, s, nrows, row0, blk, stride, out=None):
+        k = np.arange(nrows)
+        gid = row0 + k if blk <= 0 else row0 + (k // blk) * stride + (k % blk)
+        ptr, rows, signs = hashing.bucket_lists(seed, gid, m, s)
+        return self.BL(m, s, ptr, rows, signs)
+
+    def rht_stages(self, seed, X, bit_lo, bit_hi, nrows, row0, apply_diag, Y, ws=None):
+        Xn = X.numpy()
+        Z = np.zeros((nrows, Xn.shape[1]))
+        Z[: Xn.shape[0]] = Xn
+        if apply_diag:
+            Z[: Xn.shape[0]] *= hadamard.diag_signs(seed, np.arange(row0, row0 + Xn.shape[0]))[:, None]
+        hadamard.fwht_stages(Z, bit_lo, bit_hi)
+        Y.copy_(torch.from_numpy(Z))
+        return Y
+
+    def sketch_dense(self, bl, X, b, alpha, SA=None, Sb=None):
+        SA.copy_(torch.from_numpy(sketch.bucket_sum(X.numpy(), bl.ptr, bl.rows, bl.signs, alpha)))
+        if b is not None:
+            Sb.copy_(torch.from_numpy(sketch.bucket_sum(b.numpy(), bl.ptr, bl.rows, bl.signs, alpha)))
+        return SA, Sb
+
+    def ordered_sum(self, parts, alpha, out=None):
+        acc = parts[0].clone()
+        for g in range(1, parts.shape[0]):
+            acc = acc + parts[g]
+        out.copy_(alpha * acc)
+        return out
+
+    def c_ns(self, n_pad, s):
+        return sketch.c_ns(n_pad, s)
+
+    def c_s(self, s):
+        return hashing.c_s(s)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, G, port, case):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=G)
+    try:
+        from paper_2105_11815_b200 import sharded
+        n, d, m, s, seed, kind = case
+        A = gen.small_int_dense(seed, n, d) if kind == "int" else np.random.default_rng(seed).standard_normal((n, d))
+        b = np.random.default_rng(seed + 1).standard_normal(n) if kind != "int" else gen.small_int_dense(seed + 1, n, 1)[:, 0]
+        ops = OracleOps()
+        L = n // G
+        At = torch.from_numpy(A[rank * L:(rank + 1) * L].copy())
+        bt = torch.from_numpy(b[rank * L:(rank + 1) * L].copy())
+        hr = sharded.ShardedHrht(seed, At, bt, n, m, s, ops=ops)
+        strip, sb, (lo, hi) = hr.run()
+        SA = sharded.gather_strips(strip, (lo, hi), m).numpy()
+        Sb = sharded.gather_strips(sb, (lo, hi), m).numpy()
+        want, wantb = sketch.rht_sketch(seed, A, b, m, s)
+        for got, ref in ((SA, want), (Sb, wantb)):
+            assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
+            if kind == "int":
+                assert np.array_equal(got, ref)
+        # plain s-hashing with uneven row blocks
+        per = (n + G - 1) // G
+        r0, r1 = min(n, rank * per), min(n, (rank + 1) * per)
+        pl = sharded.ShardedPlain(seed, torch.from_numpy(A[r0:r1].copy()), torch.from_numpy(b[r0:r1].copy()), n, m,
+                                  s, ops=ops)
+        strip, sb, (lo, hi) = pl.run()
+        SA = sharded.gather_strips(strip, (lo, hi), m).numpy()
+        Sb = sharded.gather_strips(sb, (lo, hi), m).numpy()
+        want, wantb = sketch.sketch_dense(seed, A, b, m, s)
+        for got, ref in ((SA, want), (Sb, wantb)):
+            assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
+            if kind == "int":
+                assert np.array_equal(got, ref)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("G,case", [(2, (256, 8, 21, 1, 5, "real")), (2, (512, 6, 40, 2, 6, "int")),
+                                    (4, (1024, 5, 33, 1, 7, "real")), (4, (256, 4, 17, 3, 8, "int"))])
+def test_sharded_gloo(G, case):
+    mp.spawn(_worker, args=(G, _free_port(), case), nprocs=G, join=True)
+
+
+def test_strip_rows():
+    from paper_2105_11815_b200 import sharded
+    mq, st = sharded.strip_rows(7168, 8)
+    assert mq == 896 and st[-1] == (6272, 7168)
+    mq, st = sharded.strip_rows(10, 4)
+    assert mq == 3 and st == [(0, 3), (3, 6), (6, 9), (9, 10)]
+    assert math.prod([1]) == 1
