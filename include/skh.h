@@ -162,10 +162,10 @@ int skh_sketch_csr(int64_t m, int32_t s,
  *     (R7); rows i >= nvalid are read as zero (zero padding, R8).
  *   X [nvalid x d] (ldx >= d), Y [nrows x d] (ldy >= d); Y may alias X
  *   (then nvalid must equal nrows).  nrows must be a multiple of 2^bit_hi.
- *   ws: scratch for the D bitmap, skh_rht_stages_workspace_bytes(nvalid, row0)
- *   bytes (may be NULL when apply_diag == 0).
+ *   ws: scratch of skh_rht_stages_workspace_bytes(nrows, nvalid, row0, d) bytes
+ *   (task counters of the fused passes, the D bitmap of the generic pass).
  * ------------------------------------------------------------------------ */
-size_t skh_rht_stages_workspace_bytes(int64_t nvalid, int64_t row0);
+size_t skh_rht_stages_workspace_bytes(int64_t nrows, int64_t nvalid, int64_t row0, int64_t d);
 /* The HBM-pass split skh_rht_stages uses for `nbits` stages on rows of length d
  * (aligned != 0: X, Y 16-byte aligned with even leading dimensions).  Writes
  * the stage count of each pass (low bits first) into bits_out[0..] and returns

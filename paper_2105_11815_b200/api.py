@@ -142,10 +142,11 @@ def rht_pass_plan(nbits, d, aligned=True):
     return [buf[i] for i in range(k)]
 
 
-def rht_stages_workspace(nvalid, row0=0, device=None):
+def rht_stages_workspace(nrows, nvalid=None, row0=0, d=1, device=None):
     lib = _lib.load()
     device = device or torch.device("cuda", torch.cuda.current_device())
-    return _workspace(lib.skh_rht_stages_workspace_bytes(int(nvalid), int(row0)), device)
+    nvalid = nrows if nvalid is None else nvalid
+    return _workspace(lib.skh_rht_stages_workspace_bytes(int(nrows), int(nvalid), int(row0), int(d)), device)
 
 
 def rht_stages(seed, X, bit_lo, bit_hi, nrows=None, row0=0, apply_diag=True, alpha=1.0, Y=None, ws=None):
@@ -160,8 +161,8 @@ def rht_stages(seed, X, bit_lo, bit_hi, nrows=None, row0=0, apply_diag=True, alp
     nrows = nvalid if nrows is None else int(nrows)
     if Y is None:
         Y = torch.empty(nrows, d, dtype=torch.float64, device=X.device)
-    if apply_diag and ws is None:
-        ws = rht_stages_workspace(nvalid, row0, X.device)
+    if ws is None:
+        ws = rht_stages_workspace(nrows, nvalid, row0, d, X.device)
     rc = lib.skh_rht_stages(int(seed) & (2**64 - 1), nrows, nvalid, int(row0), d, _ptr(X), _ld(X), _ptr(Y), _ld(Y),
                             int(bit_lo), int(bit_hi), int(bool(apply_diag)), float(alpha), _ptr(ws),
                             0 if ws is None else ws.numel(), _stream())

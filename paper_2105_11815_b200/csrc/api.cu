@@ -40,10 +40,11 @@ int check_launch(const char* what) {
 // fwht.cu
 std::vector<int> plan_passes(int L, bool fast);
 bool fwht_fast_ok(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t d);
-int launch_diag_words(uint64_t seed, int64_t nvalid, int64_t row0, void* ws, cudaStream_t st);
-int launch_fwht_pass_range(int K, bool fast, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nrows,
-                           int64_t nvalid, int lo, int64_t d, int64_t g_begin, int64_t g_count, const void* dw,
-                           int64_t row0, int apply_diag, double alpha, cudaStream_t st);
+int launch_diag_words(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, int64_t d, void* ws,
+                      cudaStream_t st);
+int launch_fwht_pass_range(uint64_t seed, int K, bool fast, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                           int64_t nrows, int64_t nvalid, int lo, int64_t d, int64_t g_begin, int64_t g_count,
+                           void* ws, int64_t row0, int apply_diag, double alpha, cudaStream_t st);
 
 namespace {
 
@@ -107,7 +108,7 @@ struct RhtWs {
   double* SA;   // host variants only
   double* Sb;
   double* bin;  // host variants only: b staged on device
-  uint64_t* dw;
+  void* dw;  // transform workspace (counters + D bitmap)
   int32_t* ptr;
   int32_t* rows;
   int8_t* signs;
@@ -129,7 +130,7 @@ RhtWs rht_layout(void* base, int64_t n, int64_t n_pad, int64_t m, int s, int64_t
   w.SA = (double*)take(sizeof(double) * (size_t)m * (size_t)d);
   w.Sb = (double*)take(sizeof(double) * (size_t)m);
   w.bin = (double*)take(sizeof(double) * (size_t)std::max<int64_t>(n, 1));
-  w.dw = (uint64_t*)take(fwht_ws_bytes(n, 0));
+  w.dw = (void*)take(fwht_ws_bytes(n_pad, n, 0, d));
   w.ptr = (int32_t*)take(sizeof(int32_t) * (size_t)(m + 1));
   w.rows = (int32_t*)take(sizeof(int32_t) * (size_t)n_pad * s);
   w.signs = (int8_t*)take((size_t)n_pad * s);
@@ -184,7 +185,7 @@ int rht_tail(uint64_t seed, int64_t n, int64_t n_pad, int L, int64_t m, int s, i
       lo += K;
       continue;
     }
-    rc = launch_fwht_pass_range(K, fast && K >= 4, w.Y, d, w.Y, d, n_pad, n_pad, lo, d, 0, n_pad >> K, w.dw, 0, 0,
+    rc = launch_fwht_pass_range(seed, K, fast && K >= 4, w.Y, d, w.Y, d, n_pad, n_pad, lo, d, 0, n_pad >> K, w.dw, 0, 0,
                                 1.0, st);
     if (rc) return rc;
     lo += K;
@@ -307,9 +308,9 @@ int skh_sketch_csr(int64_t m, int32_t s, const int32_t* bucket_ptr, const int32_
   return rc;
 }
 
-size_t skh_rht_stages_workspace_bytes(int64_t nvalid, int64_t row0) {
-  if (nvalid < 0 || row0 < 0) return 0;
-  return fwht_ws_bytes(nvalid, row0);
+size_t skh_rht_stages_workspace_bytes(int64_t nrows, int64_t nvalid, int64_t row0, int64_t d) {
+  if (nrows < 0 || nvalid < 0 || row0 < 0 || d < 1) return 0;
+  return fwht_ws_bytes(nrows, nvalid, row0, d);
 }
 
 int skh_rht_pass_plan(int nbits, int64_t d, int aligned, int* bits_out, int max_out) {
@@ -336,8 +337,8 @@ int skh_rht_stages(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, i
     set_error("rht_stages: ldx/ldy < d, or in place with nvalid != nrows");
     return SKH_EDIM;
   }
-  if (apply_diag && (!ws || ws_bytes < fwht_ws_bytes(nvalid, row0))) {
-    set_error("rht_stages workspace too small: need %zu bytes", fwht_ws_bytes(nvalid, row0));
+  if (!ws || ws_bytes < fwht_ws_bytes(nrows, nvalid, row0, d)) {
+    set_error("rht_stages workspace too small: need %zu bytes", fwht_ws_bytes(nrows, nvalid, row0, d));
     return SKH_EWORKSPACE;
   }
   return launch_fwht(seed, nrows, nvalid, row0, d, X, ldx, Y, ldy, bit_lo, bit_hi, apply_diag, alpha, ws,
@@ -424,7 +425,7 @@ int skh_rht_dense_host(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d
   cudaStreamWaitEvent(cs, ev, 0);
   rc = launch_hash(seed, m, s, n_pad, 0, 0, 0, nullptr, nullptr, w.ptr, w.rows, w.signs, w.hws,
                    hash_ws_bytes(n_pad, m, s), st);
-  if (!rc) rc = launch_diag_words(seed, n, 0, w.dw, st);
+  if (!rc && !(fast && K0 >= 4)) rc = launch_diag_words(seed, n_pad, n, 0, d, w.dw, st);
   // chunked H2D into Y overlapped with the first pass (its groups are 2^K0 consecutive rows)
   const int64_t grp = (int64_t)1 << K0;
   int64_t chunk = std::max<int64_t>(grp, ((int64_t)(256ll << 20) / (8 * d)) / grp * grp);
@@ -438,12 +439,12 @@ int skh_rht_dense_host(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d
     cudaEventRecord(ev, cs);
     cudaStreamWaitEvent(st, ev, 0);
     const int64_t g0 = r0 / grp, gc = (nr + grp - 1) / grp;
-    rc = launch_fwht_pass_range(K0, fast && K0 >= 4, w.Y, d, w.Y, d, n_pad, n, 0, d, g0, gc, w.dw, 0, 1, 1.0, st);
+    rc = launch_fwht_pass_range(seed, K0, fast && K0 >= 4, w.Y, d, w.Y, d, n_pad, n, 0, d, g0, gc, w.dw, 0, 1, 1.0, st);
   }
   if (!rc && n < n_pad) {  // groups entirely in the zero padding
     const int64_t g0 = (n + grp - 1) / grp, gc = (n_pad >> K0) - g0;
     if (gc > 0)
-      rc = launch_fwht_pass_range(K0, fast && K0 >= 4, w.Y, d, w.Y, d, n_pad, n, 0, d, g0, gc, w.dw, 0, 1, 1.0, st);
+      rc = launch_fwht_pass_range(seed, K0, fast && K0 >= 4, w.Y, d, w.Y, d, n_pad, n, 0, d, g0, gc, w.dw, 0, 1, 1.0, st);
   }
   if (!rc && b_host) {
     if (cudaMemcpyAsync(w.bin, b_host, sizeof(double) * n, cudaMemcpyHostToDevice, st) != cudaSuccess)

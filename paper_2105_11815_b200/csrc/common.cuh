@@ -66,7 +66,7 @@ int launch_gather_csr(int64_t m, const int32_t* ptr, const int32_t* rows, const 
                       int64_t d, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
                       double* SA, int64_t ldsa, double alpha, cudaStream_t st);
 // fwht.cu
-size_t fwht_ws_bytes(int64_t nrows, int64_t row0);
+size_t fwht_ws_bytes(int64_t nrows, int64_t nvalid, int64_t row0, int64_t d);
 int launch_fwht(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, int64_t d,
                 const double* X, int64_t ldx, double* Y, int64_t ldy, int bit_lo, int bit_hi,
                 int apply_diag, double alpha, void* ws, cudaStream_t st);

@@ -2,51 +2,102 @@
 // row index of a row-major n x d matrix (Def. def::HRHT, PAPER.md L790-801;
 // DESIGN.md R7-R9).
 //
-// The transform over bits [bit_lo, bit_hi) is split into HBM passes of K <= 8
-// bits.  A pass over bits [lo, lo+K) is a set of independent work items
-// (group, column tile): the 2^K rows r = hi*2^(lo+K) + mid*2^lo + low
-// (mid = 0..2^K-1) restricted to TC = 2^(13-K) columns, i.e. 64 KiB of fp64.
-// Each item is loaded once (16-byte loads, 16 rows per thread), transformed in
-// registers (mid bits 0..3), exchanged once through shared memory, transformed
-// again (mid bits 4..K-1), scaled and stored once.  Stages run low bit to high
-// bit everywhere, the oracle's order, so results are bit-identical to it.
-// D is fused into the first pass (sign flip from a per-call bitmap of the
-// splitmix64 words u(key_DIAG, g >> 6)); zero padding rows are never read.
+// The transform over bits [bit_lo, bit_hi) is split into HBM passes of K bits.
+// A pass over bits [lo, lo+K) is a set of independent tiles (group, column
+// tile): the 2^K rows r = hi*2^(lo+K) + mid*2^lo + low (mid = 0..2^K-1)
+// restricted to TC columns.  A tile is loaded once with 16-byte loads (16 rows x
+// one column pair per thread, so 16 loads in flight per thread), transformed in
+// registers 4 bits at a time, re-distributed through shared memory between
+// 4-bit phases, scaled and stored once: every element crosses HBM exactly twice
+// per pass.  Stages run low bit to high bit everywhere -- the oracle's order --
+// so results are bit-identical to it.  D is fused into the first pass as a sign
+// flip; its bits come from a per-call bitmap of the splitmix64 words
+// u(key_DIAG, g >> 6), loaded before the data so the 16 data loads stay in
+// flight together.  Zero padding rows are never read.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace skh {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kGenThreads = 256;
 
-__device__ __forceinline__ bool diag_neg(const uint64_t* __restrict__ dw, int64_t w0, int64_t grow) {
-  return (dw[(grow >> 6) - w0] >> (grow & 63)) & 1ull;
-}
+int wide_mode();
 
 __global__ void diag_words_kernel(uint64_t key, int64_t w0, int64_t nw, uint64_t* __restrict__ out) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q < nw) out[q] = stream_u(key, (uint64_t)(w0 + q));
 }
 
-__device__ __forceinline__ double2 neg2(double2 a) { return make_double2(-a.x, -a.y); }
 __device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 sub2(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 
-// Fast pass: K in [4, 8], TC = 2^(13-K) columns, 16-byte aligned X/Y, even ld, even d.
+// mid index of value v (0..15) of row-slot rs in phase P of a K-bit tile.
+template <int K, int P>
+__device__ __forceinline__ int mid_of(int rs, int v) {
+  constexpr int LB = 4 * P;
+  constexpr int BP = (K - LB) < 4 ? (K - LB) : 4;
+  constexpr int J = 1 << BP;
+  constexpr int NG = 16 / J;
+  const int g = v / J, j = v % J;
+  const int other = rs * NG + g;
+  return (other & ((1 << LB) - 1)) | (j << LB) | ((other >> LB) << (LB + BP));
+}
+
+template <int K, int P>
+__device__ __forceinline__ void phase_stages(double2 (&x)[16]) {
+  constexpr int LB = 4 * P;
+  constexpr int BP = (K - LB) < 4 ? (K - LB) : 4;
+#pragma unroll
+  for (int bb = 0; bb < BP; ++bb) {
+    const int h = 1 << bb;
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {
+      if (!(v & h)) {
+        const double2 a = x[v], b = x[v + h];
+        x[v] = add2(a, b);
+        x[v + h] = sub2(a, b);
+      }
+    }
+  }
+}
+
+template <int K, int P, int CP>
+__device__ __forceinline__ void exchange(double2 (&x)[16], double2* tile, int cp, int rs) {
+#pragma unroll
+  for (int v = 0; v < 16; ++v) tile[mid_of<K, P>(rs, v) * CP + cp] = x[v];
+  __syncthreads();
+#pragma unroll
+  for (int v = 0; v < 16; ++v) x[v] = tile[mid_of<K, P + 1>(rs, v) * CP + cp];
+  __syncthreads();
+}
+
 template <int K>
-__global__ void __launch_bounds__(kThreads) fwht_fast_kernel(
+__host__ __device__ constexpr int tile_cols() {
+  return (1 << (13 - K)) > 64 ? 64 : ((1 << (13 - K)) < 8 ? 8 : (1 << (13 - K)));
+}
+template <int K>
+__host__ __device__ constexpr int tile_threads() {
+  return (1 << K) * tile_cols<K>() / 32;
+}
+
+// Fast pass: K in [4, 11]; X/Y 16-byte aligned, even ld, even d.
+template <int K, bool DIAG>
+__global__ void __launch_bounds__(tile_threads<K>()) fwht_tile_kernel(
     const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy, int64_t nvalid, int lo,
-    int64_t d, int64_t ntc, int64_t g_begin, const uint64_t* __restrict__ dw, int64_t row0, int64_t w0,
-    int apply_diag, double alpha) {
-  constexpr int TC = 1 << (13 - K);
+    int64_t d, int64_t ntc, int64_t g_begin, uint64_t dkey, int64_t row0, double alpha) {
+  constexpr int TC = tile_cols<K>();
   constexpr int CP = TC / 2;
-  constexpr int RS = kThreads / CP;  // = 2^(K-4)
-  constexpr int NB = 16 / RS;        // bsel values per thread in phase 2
+  constexpr int NPH = (K + 3) / 4;
   extern __shared__ double2 tile[];  // [2^K][CP]
   const int cp = threadIdx.x % CP, rs = threadIdx.x / CP;
   const int64_t g = g_begin + blockIdx.x / ntc;
@@ -57,82 +108,325 @@ __global__ void __launch_bounds__(kThreads) fwht_fast_kernel(
   const int64_t c = tc * TC + 2 * cp;
   const bool cv = c < d;
 
-  double2 v[16];
+  // D signs computed in registers from the splitmix64 words (no memory dependency
+  // ahead of the data loads).  Phase-0 rows of a thread are 16 consecutive rows
+  // when lo == 0, so two words cover them.
+  uint32_t negmask = 0;
+  if (DIAG) {
+    if (lo == 0) {
+      const int64_t g0 = row0 + rbase + mid_of<K, 0>(rs, 0);
+      const uint64_t wa = stream_u(dkey, (uint64_t)(g0 >> 6)), wb = stream_u(dkey, (uint64_t)((g0 + 15) >> 6));
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int64_t r = rbase + ((int64_t)(rs * 16 + j) << lo);
-    double2 x = make_double2(0.0, 0.0);
-    if (cv && r < nvalid) {
-      x = __ldg(reinterpret_cast<const double2*>(X + r * ldx + c));
-      if (apply_diag && diag_neg(dw, w0, row0 + r)) x = neg2(x);
-    }
-    v[j] = x;
-  }
+      for (int v = 0; v < 16; ++v) {
+        const int64_t gr = g0 + v;
+        const uint64_t w = ((gr >> 6) == (g0 >> 6)) ? wa : wb;
+        if (gr - row0 < nvalid) negmask |= (uint32_t)((w >> (gr & 63)) & 1ull) << v;
+      }
+    } else {
 #pragma unroll
-  for (int bb = 0; bb < 4; ++bb) {
-    const int h = 1 << bb;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (!(j & h)) {
-        const double2 a = v[j], b = v[j + h];
-        v[j] = add2(a, b);
-        v[j + h] = sub2(a, b);
+      for (int v = 0; v < 16; ++v) {
+        const int64_t r = rbase + ((int64_t)mid_of<K, 0>(rs, v) << lo);
+        const int64_t gr = row0 + r;
+        if (r < nvalid) negmask |= (uint32_t)((stream_u(dkey, (uint64_t)(gr >> 6)) >> (gr & 63)) & 1ull) << v;
       }
     }
   }
-  if (K == 4) {
-    if (cv) {
+  double2 x[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int64_t r = rbase + ((int64_t)(rs * 16 + j) << lo);
-        *reinterpret_cast<double2*>(Y + r * ldy + c) = make_double2(alpha * v[j].x, alpha * v[j].y);
-      }
-    }
-    return;
+  for (int v = 0; v < 16; ++v) {
+    const int64_t r = rbase + ((int64_t)mid_of<K, 0>(rs, v) << lo);
+    x[v] = (cv && r < nvalid) ? __ldg(reinterpret_cast<const double2*>(X + r * ldx + c)) : make_double2(0.0, 0.0);
   }
+  if (DIAG) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j) tile[(rs * 16 + j) * CP + cp] = v[j];
-  __syncthreads();
-  // phase 2: thread holds mid = a*16 + (rs*NB + t), a = 0..RS-1, t = 0..NB-1
-#pragma unroll
-  for (int t = 0; t < NB; ++t)
-#pragma unroll
-    for (int a = 0; a < RS; ++a) v[t * RS + a] = tile[(a * 16 + rs * NB + t) * CP + cp];
-#pragma unroll
-  for (int bb = 0; bb < K - 4; ++bb) {
-    const int h = 1 << bb;
-#pragma unroll
-    for (int t = 0; t < NB; ++t)
-#pragma unroll
-      for (int a = 0; a < RS; ++a) {
-        if (!(a & h)) {
-          const double2 x = v[t * RS + a], y = v[t * RS + a + h];
-          v[t * RS + a] = add2(x, y);
-          v[t * RS + a + h] = sub2(x, y);
-        }
-      }
+    for (int v = 0; v < 16; ++v)
+      if ((negmask >> v) & 1u) x[v] = make_double2(-x[v].x, -x[v].y);
+  }
+  phase_stages<K, 0>(x);
+  if constexpr (NPH > 1) {
+    exchange<K, 0, CP>(x, tile, cp, rs);
+    phase_stages<K, 1>(x);
+  }
+  if constexpr (NPH > 2) {
+    exchange<K, 1, CP>(x, tile, cp, rs);
+    phase_stages<K, 2>(x);
   }
   if (cv) {
 #pragma unroll
-    for (int t = 0; t < NB; ++t)
+    for (int v = 0; v < 16; ++v) {
+      const int64_t r = rbase + ((int64_t)mid_of<K, NPH - 1>(rs, v) << lo);
+      *reinterpret_cast<double2*>(Y + r * ldy + c) = make_double2(alpha * x[v].x, alpha * x[v].y);
+    }
+  }
+}
+
+// Cluster pass: K = KL + CB bits on a thread-block cluster of C = 2^CB CTAs.
+// CTA q holds the rows whose top CB mid bits equal q (2^KL rows x TC columns,
+// 64 KiB); it runs the KL local bits exactly like fwht_tile_kernel, then one
+// all-to-all through distributed shared memory (remote st.shared::cluster)
+// gives every CTA all C values of the top bits for 2^KL / C of the low mids,
+// and the CB cross stages finish in registers.  HBM sees one read and one
+// write per element for all K bits, with 512 B (KL=7) row segments.
+template <int KL, int CB, bool DIAG>
+__global__ void __launch_bounds__(tile_threads<KL>()) fwht_cluster_kernel(
+    const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy, int64_t nvalid, int lo,
+    int64_t d, int64_t ntc, int64_t g_begin, uint64_t dkey, int64_t row0, double alpha) {
+  constexpr int K = KL + CB;
+  constexpr int C = 1 << CB;
+  constexpr int TC = tile_cols<KL>();
+  constexpr int CP = TC / 2;
+  constexpr int NPH = (KL + 3) / 4;
+  constexpr int ML = 1 << KL;
+  constexpr int MP = ML / C;  // low-mid values owned by each CTA in the cross phase
+  constexpr int NT = 16 / C;  // low-mid values per thread in the cross phase
+  extern __shared__ double2 tile[];  // [2^KL][CP]
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = (int)cluster.block_rank();
+  const int cp = threadIdx.x % CP, rs = threadIdx.x / CP;
+  const int64_t cid = blockIdx.x / C;
+  const int64_t g = g_begin + cid / ntc;
+  const int64_t tc = cid % ntc;
+  const int64_t low = g & (((int64_t)1 << lo) - 1);
+  const int64_t hi = g >> lo;
+  const int64_t rbase = (hi << (lo + K)) + low;
+  const int64_t c = tc * TC + 2 * cp;
+  const bool cv = c < d;
+
+  uint32_t negmask = 0;
+  if (DIAG) {
+    if (lo == 0) {
+      const int64_t g0 = row0 + rbase + q * ML + mid_of<KL, 0>(rs, 0);
+      const uint64_t wa = stream_u(dkey, (uint64_t)(g0 >> 6)), wb = stream_u(dkey, (uint64_t)((g0 + 15) >> 6));
 #pragma unroll
-      for (int a = 0; a < RS; ++a) {
-        const int mid = a * 16 + rs * NB + t;
+      for (int v = 0; v < 16; ++v) {
+        const int64_t gr = g0 + v;
+        const uint64_t w = ((gr >> 6) == (g0 >> 6)) ? wa : wb;
+        if (gr - row0 < nvalid) negmask |= (uint32_t)((w >> (gr & 63)) & 1ull) << v;
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 16; ++v) {
+        const int64_t r = rbase + ((int64_t)(q * ML + mid_of<KL, 0>(rs, v)) << lo);
+        const int64_t gr = row0 + r;
+        if (r < nvalid) negmask |= (uint32_t)((stream_u(dkey, (uint64_t)(gr >> 6)) >> (gr & 63)) & 1ull) << v;
+      }
+    }
+  }
+  double2 x[16];
+#pragma unroll
+  for (int v = 0; v < 16; ++v) {
+    const int64_t r = rbase + ((int64_t)(q * ML + mid_of<KL, 0>(rs, v)) << lo);
+    x[v] = (cv && r < nvalid) ? __ldg(reinterpret_cast<const double2*>(X + r * ldx + c)) : make_double2(0.0, 0.0);
+  }
+  if (DIAG) {
+#pragma unroll
+    for (int v = 0; v < 16; ++v)
+      if ((negmask >> v) & 1u) x[v] = make_double2(-x[v].x, -x[v].y);
+  }
+  phase_stages<KL, 0>(x);
+  if constexpr (NPH > 1) {
+    exchange<KL, 0, CP>(x, tile, cp, rs);
+    phase_stages<KL, 1>(x);
+  }
+  if constexpr (NPH > 2) {
+    exchange<KL, 1, CP>(x, tile, cp, rs);
+    phase_stages<KL, 2>(x);
+  }
+  // cross-CTA all-to-all: value for low-mid m goes to CTA m / MP, slot (m % MP) * C + q
+  cluster.sync();  // every CTA has finished reading its own tile buffer
+#pragma unroll
+  for (int v = 0; v < 16; ++v) {
+    const int m = mid_of<KL, NPH - 1>(rs, v);
+    double2* dst = cluster.map_shared_rank(tile, m / MP);
+    dst[((m % MP) * C + q) * CP + cp] = x[v];
+  }
+  cluster.sync();  // all remote stores landed
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int qq = 0; qq < C; ++qq) x[t * C + qq] = tile[((rs * NT + t) * C + qq) * CP + cp];
+#pragma unroll
+  for (int bb = 0; bb < CB; ++bb) {
+    const int h = 1 << bb;
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int qq = 0; qq < C; ++qq)
+        if (!(qq & h)) {
+          const double2 a = x[t * C + qq], b = x[t * C + qq + h];
+          x[t * C + qq] = add2(a, b);
+          x[t * C + qq + h] = sub2(a, b);
+        }
+  }
+  if (cv) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int qq = 0; qq < C; ++qq) {
+        const int mid = qq * ML + q * MP + rs * NT + t;
         const int64_t r = rbase + ((int64_t)mid << lo);
-        const double2 x = v[t * RS + a];
-        *reinterpret_cast<double2*>(Y + r * ldy + c) = make_double2(alpha * x.x, alpha * x.y);
+        const double2 v = x[t * C + qq];
+        *reinterpret_cast<double2*>(Y + r * ldy + c) = make_double2(alpha * v.x, alpha * v.y);
       }
   }
 }
 
-// Generic pass: any d, any alignment, K in [0, 6]; one thread per (group, column).
+// Fused pass through L2: K = 7 + KB bits with one HBM read and one HBM write.
+// A unit (group of 2^K rows x 64 columns, 2^K * 512 B) is split into 2^KB
+// A-tasks (a 7-bit tile over the low mid bits, exactly fwht_tile_kernel<7>) and
+// 2^KB B-tasks (the KB high mid bits for 128 / 2^KB low-mid values, all in
+// registers).  A persistent grid pulls tasks from an atomic counter in an
+// order that interleaves A-tasks of unit u with B-tasks of unit u - LAG; a
+// B-task waits (acquire) until the unit's A-tasks have published (release)
+// their stores, then reads them with ld.global.cg -- from L2, where they still
+// are because only ~LAG units (tens of MiB) are in flight.  B-tasks never block
+// A-tasks and tasks are claimed in dependency order, so the schedule cannot
+// deadlock whatever the residency.  Stage order stays low bit -> high bit.
+template <int KB, bool DIAG>
+__global__ void __launch_bounds__(256) fwht_fused_kernel(
+    const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy, int64_t nvalid, int lo,
+    int64_t d, int64_t ntc, int64_t g_begin, int64_t nunits, int64_t lag, uint32_t* __restrict__ counters,
+    uint64_t dkey, int64_t row0, double alpha) {
+  constexpr int K = 7 + KB;
+  constexpr int TC = 64, CP = 32;
+  constexpr int NB = 1 << KB;       // A-tasks (and B-tasks) per unit
+  constexpr int NA = 16 / NB;       // low-mid values per thread in a B-task
+  extern __shared__ double2 tile[];  // [128][CP]
+  __shared__ int64_t s_task;
+  uint32_t* task_ctr = counters;
+  uint32_t* done = counters + 64;
+  const int cp = threadIdx.x % CP, rs = threadIdx.x / CP;
+  const int64_t lagc = lag < nunits ? lag : nunits;
+  const int64_t nblocks = 2 * nunits;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = (int64_t)atomicAdd(task_ctr, 1u);
+    __syncthreads();
+    const int64_t t = s_task;
+    __syncthreads();
+    if (t >= nblocks * NB) break;
+    // decode: block k = t / NB; blocks A_0..A_{lag-1}, then (A_{lag+i}, B_i) pairs, then the last B's
+    const int64_t k = t / NB;
+    const int sub = (int)(t % NB);
+    int64_t u;
+    bool isA;
+    if (k < lagc) {
+      u = k;
+      isA = true;
+    } else if (k < lagc + 2 * (nunits - lagc)) {
+      const int64_t j = k - lagc;
+      isA = (j & 1) == 0;
+      u = isA ? lagc + j / 2 : j / 2;
+    } else {
+      isA = false;
+      u = (nunits - lagc) + (k - lagc - 2 * (nunits - lagc));
+    }
+    const int64_t g = g_begin + u / ntc;
+    const int64_t tc = u % ntc;
+    const int64_t low = g & (((int64_t)1 << lo) - 1);
+    const int64_t hi = g >> lo;
+    const int64_t rbase = (hi << (lo + K)) + low;
+    const int64_t c = tc * TC + 2 * cp;
+    const bool cv = c < d;
+    double2 x[16];
+    if (isA) {
+      // rows mid = a + 128 * sub, a = 0..127 (a 7-bit tile)
+      const int64_t rb = rbase + ((int64_t)(sub * 128) << lo);
+      uint32_t negmask = 0;
+      if (DIAG) {
+        if (lo == 0) {
+          const int64_t g0 = row0 + rb + mid_of<7, 0>(rs, 0);
+          const uint64_t wa = stream_u(dkey, (uint64_t)(g0 >> 6)), wb = stream_u(dkey, (uint64_t)((g0 + 15) >> 6));
+#pragma unroll
+          for (int v = 0; v < 16; ++v) {
+            const int64_t gr = g0 + v;
+            const uint64_t w = ((gr >> 6) == (g0 >> 6)) ? wa : wb;
+            if (gr - row0 < nvalid) negmask |= (uint32_t)((w >> (gr & 63)) & 1ull) << v;
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < 16; ++v) {
+            const int64_t r = rb + ((int64_t)mid_of<7, 0>(rs, v) << lo);
+            const int64_t gr = row0 + r;
+            if (r < nvalid) negmask |= (uint32_t)((stream_u(dkey, (uint64_t)(gr >> 6)) >> (gr & 63)) & 1ull) << v;
+          }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 16; ++v) {
+        const int64_t r = rb + ((int64_t)mid_of<7, 0>(rs, v) << lo);
+        x[v] = (cv && r < nvalid) ? __ldg(reinterpret_cast<const double2*>(X + r * ldx + c))
+                                  : make_double2(0.0, 0.0);
+      }
+      if (DIAG) {
+#pragma unroll
+        for (int v = 0; v < 16; ++v)
+          if ((negmask >> v) & 1u) x[v] = make_double2(-x[v].x, -x[v].y);
+      }
+      phase_stages<7, 0>(x);
+      exchange<7, 0, CP>(x, tile, cp, rs);
+      phase_stages<7, 1>(x);
+      if (cv) {
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          const int64_t r = rb + ((int64_t)mid_of<7, 1>(rs, v) << lo);
+          *reinterpret_cast<double2*>(Y + r * ldy + c) = x[v];
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicAdd(done + u, 1u);
+    } else {
+      if (threadIdx.x == 0) {
+        unsigned ns = 32;
+        for (;;) {
+          uint32_t v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done + u) : "memory");
+          if (v >= (uint32_t)NB) break;
+          __nanosleep(ns);
+          if (ns < 1024) ns *= 2;
+        }
+      }
+      __syncthreads();
+      // value v = aa * NB + b: low mid a = sub * (128 / NB) + rs * NA + aa, high bits b
+#pragma unroll
+      for (int v = 0; v < 16; ++v) {
+        const int aa = v / NB, b = v % NB;
+        const int mid = sub * (128 / NB) + rs * NA + aa + 128 * b;
+        const int64_t r = rbase + ((int64_t)mid << lo);
+        x[v] = cv ? __ldcg(reinterpret_cast<const double2*>(Y + r * ldy + c)) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int bb = 0; bb < KB; ++bb) {
+        const int h = 1 << bb;
+#pragma unroll
+        for (int v = 0; v < 16; ++v)
+          if (!(v & h)) {
+            const double2 a = x[v], b = x[v + h];
+            x[v] = add2(a, b);
+            x[v + h] = sub2(a, b);
+          }
+      }
+      if (cv) {
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          const int aa = v / NB, b = v % NB;
+          const int mid = sub * (128 / NB) + rs * NA + aa + 128 * b;
+          const int64_t r = rbase + ((int64_t)mid << lo);
+          *reinterpret_cast<double2*>(Y + r * ldy + c) = make_double2(alpha * x[v].x, alpha * x[v].y);
+        }
+      }
+    }
+  }
+}
+
+// Generic pass: any d, any alignment, K in [0, 5]; one thread per (group, column).
 template <int K>
-__global__ void __launch_bounds__(kThreads) fwht_generic_kernel(
+__global__ void __launch_bounds__(kGenThreads) fwht_generic_kernel(
     const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy, int64_t nvalid, int lo,
     int64_t d, int64_t g_begin, int64_t ngroups, const uint64_t* __restrict__ dw, int64_t row0, int64_t w0,
     int apply_diag, double alpha) {
   constexpr int R = 1 << K;
-  const int64_t idx = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int64_t idx = (int64_t)blockIdx.x * kGenThreads + threadIdx.x;
   if (idx >= ngroups * d) return;
   const int64_t c = idx % d;
   const int64_t g = g_begin + idx / d;
@@ -140,15 +434,21 @@ __global__ void __launch_bounds__(kThreads) fwht_generic_kernel(
   const int64_t hi = g >> lo;
   const int64_t rbase = (hi << (lo + K)) + low;
   double v[R];
+  uint64_t wv[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     const int64_t r = rbase + ((int64_t)j << lo);
-    double x = 0.0;
-    if (r < nvalid) {
-      x = X[r * ldx + c];
-      if (apply_diag && diag_neg(dw, w0, row0 + r)) x = -x;
-    }
-    v[j] = x;
+    wv[j] = (apply_diag && r < nvalid) ? dw[((row0 + r) >> 6) - w0] : 0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int64_t r = rbase + ((int64_t)j << lo);
+    v[j] = r < nvalid ? X[r * ldx + c] : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int64_t r = rbase + ((int64_t)j << lo);
+    if ((wv[j] >> ((row0 + r) & 63)) & 1ull) v[j] = -v[j];
   }
 #pragma unroll
   for (int bb = 0; bb < K; ++bb) {
@@ -165,77 +465,233 @@ __global__ void __launch_bounds__(kThreads) fwht_generic_kernel(
   for (int j = 0; j < R; ++j) Y[(rbase + ((int64_t)j << lo)) * ldy + c] = alpha * v[j];
 }
 
-template <int K>
-int launch_fast(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nrows, int64_t nvalid, int lo,
-                int64_t d, int64_t g_begin, int64_t g_count, const uint64_t* dw, int64_t row0, int64_t w0,
-                int apply_diag, double alpha, cudaStream_t st) {
-  constexpr int TC = 1 << (13 - K);
+template <int K, bool DIAG>
+int launch_tile(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo, int64_t d,
+                int64_t g_begin, int64_t g_count, uint64_t dkey, int64_t row0, double alpha, cudaStream_t st) {
+  constexpr int TC = tile_cols<K>();
+  constexpr int T = tile_threads<K>();
   const size_t smem = (size_t)(1 << K) * TC * sizeof(double);
-  cudaFuncSetAttribute(fwht_fast_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(fwht_tile_kernel<K, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntc = (d + TC - 1) / TC;
-  (void)nrows;
-  // chunk the grid so every launch has < 2^31 CTAs
-  const int64_t max_groups = ((1ll << 31) - 1) / ntc;
+  const int64_t max_groups = ((1ll << 31) - 1) / ntc;  // keep every grid below 2^31 CTAs
   for (int64_t g0 = g_begin; g0 < g_begin + g_count; g0 += max_groups) {
-    const int64_t gc = min(max_groups, g_begin + g_count - g0);
-    fwht_fast_kernel<K><<<(unsigned)(gc * ntc), kThreads, smem, st>>>(X, ldx, Y, ldy, nvalid, lo, d, ntc, g0, dw,
-                                                                      row0, w0, apply_diag, alpha); note_launch();
+    const int64_t gc = std::min(max_groups, g_begin + g_count - g0);
+    fwht_tile_kernel<K, DIAG><<<(unsigned)(gc * ntc), T, smem, st>>>(X, ldx, Y, ldy, nvalid, lo, d, ntc, g0, dkey,
+                                                                      row0, alpha);
+    note_launch();
   }
-  return check_launch("fwht_fast");
+  return check_launch("fwht_tile");
+}
+
+template <int KL, int CB, bool DIAG>
+int launch_cluster(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo, int64_t d,
+                   int64_t g_begin, int64_t g_count, uint64_t dkey, int64_t row0, double alpha, cudaStream_t st) {
+  constexpr int TC = tile_cols<KL>();
+  constexpr int T = tile_threads<KL>();
+  constexpr int C = 1 << CB;
+  const size_t smem = (size_t)(1 << KL) * TC * sizeof(double);
+  auto kern = fwht_cluster_kernel<KL, CB, DIAG>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  const int64_t ntc = (d + TC - 1) / TC;
+  const int64_t max_groups = ((1ll << 31) - 1) / (ntc * C);
+  for (int64_t g0 = g_begin; g0 < g_begin + g_count; g0 += max_groups) {
+    const int64_t gc = std::min(max_groups, g_begin + g_count - g0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(gc * ntc * C), 1, 1);
+    cfg.blockDim = dim3(T, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, X, ldx, Y, ldy, nvalid, lo, d, ntc, g0, dkey, row0, alpha);
+    note_launch();
+    if (e != cudaSuccess) {
+      set_error("fwht_cluster launch: %s", cudaGetErrorString(e));
+      return SKH_ECUDA;
+    }
+  }
+  return check_launch("fwht_cluster");
+}
+
+// K in [9, 11]: local bits KL (TC = 64 for KL = 7, 32 for KL = 8) + CB cross bits.
+int launch_cluster_k(int K, bool diag, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo,
+                     int64_t d, int64_t g_begin, int64_t g_count, uint64_t dkey, int64_t row0, double alpha,
+                     cudaStream_t st) {
+#define SKH_CL(KL, CB)                                                                                               \
+  return diag ? launch_cluster<KL, CB, true>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dkey, row0, alpha, st) \
+              : launch_cluster<KL, CB, false>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dkey, row0, alpha, st)
+  switch (K) {
+    case 9: SKH_CL(7, 2);
+    case 10: SKH_CL(7, 3);
+    case 11: SKH_CL(8, 3);
+    default: break;
+  }
+#undef SKH_CL
+  set_error("internal: bad cluster pass width %d", K);
+  return SKH_EINVAL;
+}
+
+int sm_count() {
+  static int v = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return v;
+}
+
+template <int KB, bool DIAG>
+int launch_fused(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo, int64_t d,
+                 int64_t g_begin, int64_t g_count, uint32_t* counters, uint64_t dkey, int64_t row0, double alpha,
+                 cudaStream_t st) {
+  constexpr int NB = 1 << KB;
+  const size_t smem = 128 * 32 * sizeof(double2);
+  auto kern = fwht_fused_kernel<KB, DIAG>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t resident = (int64_t)per_sm * sm_count();
+  const int64_t ntc = (d + 63) / 64;
+  const int64_t nunits = g_count * ntc;
+  const int64_t ntasks = 2 * nunits * NB;
+  const int64_t lag = std::max<int64_t>(1, (resident + 2 * NB - 1) / (2 * NB));
+  const int64_t grid = std::min<int64_t>(resident, ntasks);
+  cudaMemsetAsync(counters, 0, sizeof(uint32_t) * (size_t)(64 + nunits), st);
+  kern<<<(unsigned)grid, 256, smem, st>>>(X, ldx, Y, ldy, nvalid, lo, d, ntc, g_begin, nunits, lag, counters, dkey,
+                                           row0, alpha);
+  note_launch();
+  return check_launch("fwht_fused");
+}
+
+int launch_fused_k(int K, bool diag, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo,
+                   int64_t d, int64_t g_begin, int64_t g_count, uint32_t* counters, uint64_t dkey, int64_t row0,
+                   double alpha, cudaStream_t st) {
+#define SKH_FU(KB)                                                                                                 \
+  return diag ? launch_fused<KB, true>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0,      \
+                                       alpha, st)                                                                  \
+              : launch_fused<KB, false>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0,     \
+                                        alpha, st)
+  switch (K) {
+    case 9: SKH_FU(2);
+    case 10: SKH_FU(3);
+    case 11: SKH_FU(4);
+    default: break;
+  }
+#undef SKH_FU
+  set_error("internal: bad fused pass width %d", K);
+  return SKH_EINVAL;
 }
 
 template <int K>
 int launch_generic(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo, int64_t d,
                    int64_t g_begin, int64_t g_count, const uint64_t* dw, int64_t row0, int64_t w0, int apply_diag,
                    double alpha, cudaStream_t st) {
-  const int64_t per = ((1ll << 31) - 1) * (int64_t)kThreads / d;  // groups per launch (grid < 2^31)
+  const int64_t per = ((1ll << 31) - 1) * (int64_t)kGenThreads / d;  // groups per launch (grid < 2^31)
   const int64_t step = per > 0 ? per : 1;
   for (int64_t g0 = g_begin; g0 < g_begin + g_count; g0 += step) {
-    const int64_t gc = min(step, g_begin + g_count - g0);
+    const int64_t gc = std::min(step, g_begin + g_count - g0);
     const int64_t threads = gc * d;
-    fwht_generic_kernel<K><<<(unsigned)((threads + kThreads - 1) / kThreads), kThreads, 0, st>>>(
-        X, ldx, Y, ldy, nvalid, lo, d, g0, gc, dw, row0, w0, apply_diag, alpha); note_launch();
+    fwht_generic_kernel<K><<<(unsigned)((threads + kGenThreads - 1) / kGenThreads), kGenThreads, 0, st>>>(
+        X, ldx, Y, ldy, nvalid, lo, d, g0, gc, dw, row0, w0, apply_diag, alpha);
+    note_launch();
   }
   return check_launch("fwht_generic");
 }
 
-int launch_pass(bool fast, int K, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nrows,
-                int64_t nvalid, int lo, int64_t d, int64_t g_begin, int64_t g_count, const uint64_t* dw,
+template <int K>
+int launch_tile_d(bool diag, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo,
+                  int64_t d, int64_t g_begin, int64_t g_count, uint64_t dkey, int64_t row0, double alpha,
+                  cudaStream_t st) {
+  return diag ? launch_tile<K, true>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dkey, row0, alpha, st)
+              : launch_tile<K, false>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dkey, row0, alpha, st);
+}
+
+int launch_pass(bool fast, int K, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo,
+                int64_t d, int64_t g_begin, int64_t g_count, const uint64_t* dw, uint32_t* counters, uint64_t dkey,
                 int64_t row0, int64_t w0, int apply_diag, double alpha, cudaStream_t st) {
+  const bool dg = apply_diag != 0;
   if (fast) {
+#define SKH_TILE(KK) \
+  case KK: return launch_tile_d<KK>(dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dkey, row0, alpha, st)
+    if (K >= 9 && K <= 11 && wide_mode() == 1)
+      return launch_fused_k(K, dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0, alpha, st);
+    if (K >= 9 && K <= 11 && wide_mode() == 2)
+      return launch_cluster_k(K, dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dkey, row0, alpha, st);
     switch (K) {
-      case 4: return launch_fast<4>(X, ldx, Y, ldy, nrows, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st);
-      case 5: return launch_fast<5>(X, ldx, Y, ldy, nrows, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st);
-      case 6: return launch_fast<6>(X, ldx, Y, ldy, nrows, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st);
-      case 7: return launch_fast<7>(X, ldx, Y, ldy, nrows, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st);
-      case 8: return launch_fast<8>(X, ldx, Y, ldy, nrows, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st);
+      SKH_TILE(4);
+      SKH_TILE(5);
+      SKH_TILE(6);
+      SKH_TILE(7);
+      SKH_TILE(8);
+      SKH_TILE(9);
+      SKH_TILE(10);
+      SKH_TILE(11);
       default: break;
     }
+#undef SKH_TILE
   }
+#define SKH_GEN(KK) \
+  case KK: return launch_generic<KK>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st)
   switch (K) {
-    case 0: return launch_generic<0>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st);
-    case 1: return launch_generic<1>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st);
-    case 2: return launch_generic<2>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st);
-    case 3: return launch_generic<3>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st);
-    case 4: return launch_generic<4>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st);
-    case 5: return launch_generic<5>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st);
-    case 6: return launch_generic<6>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dw, row0, w0, apply_diag, alpha, st);
+    SKH_GEN(0);
+    SKH_GEN(1);
+    SKH_GEN(2);
+    SKH_GEN(3);
+    SKH_GEN(4);
+    SKH_GEN(5);
     default: break;
   }
+#undef SKH_GEN
   set_error("internal: bad pass width %d", K);
   return SKH_EINVAL;
 }
 
+int kmax_fast() {
+  // Widest pass used by the planner.  Default 8: single-CTA tile
+  // passes run at the HBM copy rate, while the 9..11-bit passes (fused through
+  // L2 or over DSMEM clusters) measured at ~0.5x of it on B200 because L2 and
+  // DSMEM move data no faster than HBM (profiles/r01).  SKH_FWHT_KMAX=9..11
+  // enables them for experiments.
+  static int v = [] {
+    const char* e = getenv("SKH_FWHT_KMAX");
+    int k = e ? atoi(e) : 8;
+    return k < 4 ? 4 : (k > 11 ? 11 : k);
+  }();
+  return v;
+}
+
+// Passes of 9..11 bits: 1 = fused through L2 (default), 2 = thread-block
+// clusters over DSMEM, 0 = single-CTA tiles (SKH_FWHT_WIDE = fused|cluster|tile).
+int wide_mode() {
+  static int v = [] {
+    const char* e = getenv("SKH_FWHT_WIDE");
+    if (!e) return 1;
+    if (e[0] == 'c') return 2;
+    if (e[0] == 't') return 0;
+    return 1;
+  }();
+  return v;
+}
+
 }  // namespace
 
-// Split L bits into passes: fast passes hold 4..8 bits, generic passes 0..6.
+// Split L bits into passes (low bits first): tile passes hold 4..kmax bits,
+// generic passes at most 5.
 std::vector<int> plan_passes(int L, bool fast) {
   std::vector<int> ks;
   if (L <= 0) {
     ks.push_back(0);
     return ks;
   }
-  const int kmax = fast ? 8 : 6;
+  const int kmax = fast ? kmax_fast() : 5;
   const int P = (L + kmax - 1) / kmax;
   for (int p = 0; p < P; ++p) ks.push_back(L / P + (p < L % P ? 1 : 0));
   return ks;
@@ -246,27 +702,42 @@ bool fwht_fast_ok(const double* X, int64_t ldx, const double* Y, int64_t ldy, in
          ldy % 2 == 0 && d % 2 == 0 && d >= 16;
 }
 
-size_t fwht_ws_bytes(int64_t nvalid, int64_t row0) {
-  if (nvalid <= 0) return 256;
-  const int64_t w0 = row0 >> 6, w1 = (row0 + nvalid - 1) >> 6;
-  return align_up(sizeof(uint64_t) * (size_t)(w1 - w0 + 1));
+// Workspace of a transform call: [task counter + per-unit counters of fused
+// passes][D bitmap for the generic first pass].
+size_t fwht_counter_bytes(int64_t nrows, int64_t d) {
+  return align_up(sizeof(uint32_t) * (size_t)(64 + std::max<int64_t>(1, (nrows >> 9) * ((d + 63) / 64))));
 }
 
-// Enqueue the diag bitmap for rows [row0, row0 + nvalid) into ws.
-int launch_diag_words(uint64_t seed, int64_t nvalid, int64_t row0, void* ws, cudaStream_t st) {
+size_t fwht_ws_bytes(int64_t nrows, int64_t nvalid, int64_t row0, int64_t d) {
+  size_t b = fwht_counter_bytes(nrows, d);
+  if (nvalid > 0) {
+    const int64_t w0 = row0 >> 6, w1 = (row0 + nvalid - 1) >> 6;
+    b += align_up(sizeof(uint64_t) * (size_t)(w1 - w0 + 1));
+  }
+  return b;
+}
+
+static uint64_t* bitmap_of(void* ws, int64_t nrows, int64_t d) {
+  return reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + fwht_counter_bytes(nrows, d));
+}
+
+// Enqueue the diag bitmap for rows [row0, row0 + nvalid) (used by generic passes).
+int launch_diag_words(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, int64_t d, void* ws,
+                      cudaStream_t st) {
   if (nvalid <= 0) return SKH_OK;
   const int64_t w0 = row0 >> 6, nw = ((row0 + nvalid - 1) >> 6) - w0 + 1;
-  diag_words_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(key_diag(seed), w0, nw, (uint64_t*)ws); note_launch();
+  diag_words_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(key_diag(seed), w0, nw, bitmap_of(ws, nrows, d));
+  note_launch();
   return check_launch("diag_words");
 }
 
 // One pass restricted to groups [g_begin, g_begin + g_count) (for chunked host input).
-int launch_fwht_pass_range(int K, bool fast, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nrows,
-                           int64_t nvalid, int lo, int64_t d, int64_t g_begin, int64_t g_count, const void* dw,
-                           int64_t row0, int apply_diag, double alpha, cudaStream_t st) {
-  if (fast && (K < 4 || K > 8)) fast = false;
-  return launch_pass(fast, K, X, ldx, Y, ldy, nrows, nvalid, lo, d, g_begin, g_count, (const uint64_t*)dw, row0,
-                     row0 >> 6, apply_diag, alpha, st);
+int launch_fwht_pass_range(uint64_t seed, int K, bool fast, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                           int64_t nrows, int64_t nvalid, int lo, int64_t d, int64_t g_begin, int64_t g_count,
+                           void* ws, int64_t row0, int apply_diag, double alpha, cudaStream_t st) {
+  if (fast && (K < 4 || K > 11)) fast = false;
+  return launch_pass(fast, K, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, bitmap_of(ws, nrows, d),
+                     static_cast<uint32_t*>(ws), key_diag(seed), row0, row0 >> 6, apply_diag, alpha, st);
 }
 
 int launch_fwht(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, int64_t d, const double* X,
@@ -274,19 +745,19 @@ int launch_fwht(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, int6
                 void* ws, cudaStream_t st) {
   const bool fast = fwht_fast_ok(X, ldx, Y, ldy, d);
   int rc;
-  if (apply_diag) {
-    rc = launch_diag_words(seed, nvalid, row0, ws, st);
+  std::vector<int> ks = plan_passes(bit_hi - bit_lo, fast);
+  if (apply_diag && !(fast && ks[0] >= 4)) {  // only the generic first pass reads the bitmap
+    rc = launch_diag_words(seed, nrows, nvalid, row0, d, ws, st);
     if (rc) return rc;
   }
-  std::vector<int> ks = plan_passes(bit_hi - bit_lo, fast);
   int lo = bit_lo;
   for (size_t p = 0; p < ks.size(); ++p) {
     const int K = ks[p];
     const bool first = p == 0, last = p + 1 == ks.size();
-    const bool f = fast && K >= 4;
     const int64_t ngroups = nrows >> K;
-    rc = launch_pass(f, K, first ? X : Y, first ? ldx : ldy, Y, ldy, nrows, first ? nvalid : nrows, lo, d, 0,
-                     ngroups, (const uint64_t*)ws, row0, row0 >> 6, first ? apply_diag : 0, last ? alpha : 1.0, st);
+    rc = launch_pass(fast && K >= 4, K, first ? X : Y, first ? ldx : ldy, Y, ldy, first ? nvalid : nrows, lo, d, 0,
+                     ngroups, bitmap_of(ws, nrows, d), static_cast<uint32_t*>(ws), key_diag(seed), row0, row0 >> 6,
+                     first ? apply_diag : 0, last ? alpha : 1.0, st);
     if (rc) return rc;
     lo += K;
   }

@@ -62,7 +62,7 @@ class HrhtStep:
         self.SA = torch.empty(self.m, d, dtype=torch.float64, device=dev)
         self.Sb = torch.empty(self.m, dtype=torch.float64, device=dev) if b is not None else None
         self.bl = None
-        self.ws = api.rht_stages_workspace(n, 0, dev)
+        self.ws = api.rht_stages_workspace(n_pad, n, 0, d, dev)
         self.alpha = api.c_ns(n_pad, s)
         names = ["hash_gen"] + [f"fwht_pass{p}" for p in range(len(self.plan))]
         if b is not None:

@@ -100,7 +100,7 @@ class ShardedHrht:
         self.alpha = self.ops.c_ns(self.n, self.s)
         self.ws = None
         if isinstance(self.ops, CudaOps):
-            self.ws = self.ops.api.rht_stages_workspace(self.L, self.r * self.L, A_loc.device)
+            self.ws = self.ops.api.rht_stages_workspace(self.L, self.L, self.r * self.L, d, A_loc.device)
 
     def run(self):
         ops, G, r, L = self.ops, self.G, self.r, self.L

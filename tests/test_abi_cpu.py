@@ -63,6 +63,7 @@ def test_error_codes(lib):
     assert lib.skh_rht_stages(1, 12, 12, 0, 4, p, 4, p, 4, 0, 3, 0, 1.0, None, 0, None) == ENOTPOW2
     assert lib.skh_rht_stages(1, 16, 12, 0, 4, p, 4, p, 4, 0, 4, 0, 1.0, None, 0, None) == EDIM
     assert lib.skh_rht_stages(1, 16, 16, 0, 4, p, 4, p, 4, 0, 4, 1, 1.0, None, 0, None) == EWS
+    assert lib.skh_rht_stages(1, 16, 16, 0, 4, p, 4, p, 4, 0, 4, 0, 1.0, p, 8, None) == EWS
     # rht_dense: workspace too small
     assert lib.skh_rht_dense(1, 100, 10, 1, 4, p, 4, None, p, 4, None, p, 16, None) == EWS
     assert b"workspace" in lib.skh_last_error()
@@ -75,7 +76,7 @@ def test_workspace_queries(lib):
     ws = lib.skh_rht_dense_workspace_bytes(n, m, s, d)
     assert ws >= n * d * 8 and ws < n * d * 8 * 1.05
     assert lib.skh_hash_workspace_bytes(1000, 10, 3) >= 2 * 8 * 3000
-    assert lib.skh_rht_stages_workspace_bytes(130, 60) >= 8 * 3
+    assert lib.skh_rht_stages_workspace_bytes(256, 130, 60, 8) >= 8 * 3 + 4 * 64
 
 
 def test_product_has_no_fallback():
