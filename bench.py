@@ -205,7 +205,7 @@ def roofline(cfg, step, stage_ms, peak_gbs, peak_src):
         t = stage_ms[name]
     elif cfg.hd:
         passes = [k for k in stage_ms if k.startswith("fwht_pass")]
-        name = "fwht_fast (" + "+".join(str(k) for k in step.plan) + " stage passes, mean per launch)"
+        name = "fwht_tile_kernel (" + "+".join(str(k) for k in step.plan) + " stage passes, mean per launch)"
         alg = 2 * step.n_pad * cfg.d * 8          # read + write the n x d block once per pass
         t = sum(stage_ms[k] for k in passes) / len(passes)
     else:
@@ -213,9 +213,16 @@ def roofline(cfg, step, stage_ms, peak_gbs, peak_src):
         alg = cfg.n * cfg.d * 8 + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5
         t = stage_ms["gather"]
     achieved = alg / (t / 1e3) / 1e9
+    traffic, tsrc = None, None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            ent = json.load(f).get(cfg.name)
+        if ent and ent["kernel"].split("<")[0] in name:
+            traffic, tsrc = ent["dram_bytes_per_launch"], ent["source"]
     return {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
-            "frac": round(achieved / peak_gbs, 4), "traffic": None, "alg_bytes_per_launch": alg,
-            "ms_per_launch": round(t, 4), "peak_source": peak_src}
+            "frac": round(achieved / peak_gbs, 4), "traffic": traffic, "traffic_source": tsrc,
+            "alg_bytes_per_launch": alg, "ms_per_launch": round(t, 4), "peak_source": peak_src}
 
 
 def gpu_arm_single(args, cfg):

@@ -4,18 +4,20 @@
 //
 // One CTA per bucket (C4: m = 16384 buckets of ~192 rows x 8 nonzeros; SA is
 // 1 GiB dense, 91 % of the bytes -- the kernel is bound by writing SA once).
-//   Stage   all 256 threads pull the bucket's rows in parallel (one row per
-//           thread per round: row id, sign, row_ptr, then its nonzeros) and pack
-//           (column, signed value) in list order into shared memory -- three
-//           dependent round trips per 256 rows instead of one per nonzero.
-//   Reduce  per column tile (<= 4096 columns of fp64 in shared memory, zero-filled
-//           in place): warp w owns 1/8 of the tile's columns and walks the packed
-//           list in order; lanes of one 32-entry step that hit the same column
-//           are combined by their lowest lane in lane order (= ascending row),
-//           so every column sees its terms in canonical order.
+//   Stage   256 rows per round, one per thread: row id + sign, then row_ptr, a
+//           block scan of the row lengths, then the nonzeros are copied in a
+//           flattened, coalesced loop (entry e finds its row by binary search
+//           in the scanned offsets) -- three dependent round trips per 256 rows,
+//           all loads of a round in flight together.  (column, signed value)
+//           pairs land in shared memory in list order.
+//   Reduce  per column tile (<= 4096 fp64 columns in shared memory, zero-filled
+//           in place): warp w owns 1/8 of the tile's columns and walks the
+//           staged list in order; lanes of one 32-entry step that hit the same
+//           column are combined by their lowest lane in lane order (= ascending
+//           row), so every column sees its terms in canonical order.
 //   Write   the tile is streamed out once with 16-byte stores.
-// Buckets larger than the staging capacity are processed in row chunks in
-// order, which keeps the summation order.
+// A bucket whose nonzeros fit the staging buffer is staged once for all column
+// tiles; larger buckets are processed in row chunks, in order.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -60,9 +62,12 @@ __global__ void __launch_bounds__(kThreads) gather_csr_kernel(
     int64_t m, const int32_t* __restrict__ ptr, const int32_t* __restrict__ brow, const int8_t* __restrict__ bsg,
     int64_t d, int tile_cols, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
     const double* __restrict__ val, double* __restrict__ SA, int64_t ldsa, double alpha) {
-  extern __shared__ double acc[];                       // [tile_cols]
+  extern __shared__ double acc[];  // [tile_cols]
   __shared__ int s_col[kStageCap];
   __shared__ double s_val[kStageCap];
+  __shared__ int r_off[kThreads + 1];  // staged offset of each row of the round (+ end)
+  __shared__ int64_t r_start[kThreads];
+  __shared__ int r_neg[kThreads];
   __shared__ double stage[kWarps][32];
   __shared__ int wsum[32];
   __shared__ int s_total;
@@ -71,79 +76,80 @@ __global__ void __launch_bounds__(kThreads) gather_csr_kernel(
   const unsigned lt = (1u << lane) - 1u;
   const int beg = ptr[b], end = ptr[b + 1];
   const int ntiles = (int)((d + tile_cols - 1) / tile_cols);
+  bool whole = false;  // the whole bucket sits in the staging buffer
+  int staged = 0;
 
-  // column tiles one after another; within a tile the rows are staged in
-  // chunks, in list order, and each chunk is reduced before the next.
   for (int t = 0; t < ntiles; ++t) {
     const int64_t c0 = (int64_t)t * tile_cols;
     const int width = (int)min((int64_t)tile_cols, d - c0);
     for (int i = threadIdx.x; i < width; i += kThreads) acc[i] = 0.0;
-    int rpos = beg;  // next row (list position) to stage
+    int rpos = beg;
     while (rpos < end) {
-      // ---- stage rows [rpos, ...) while they fit kStageCap nonzeros
-      int staged = 0;
       int rnext = rpos;
-      while (rnext < end) {
-        const int tr = rnext + (int)threadIdx.x;
-        int len = 0, neg = 0;
-        int64_t rs = 0;
-        if (tr < end) {
-          const int r = brow[tr];
-          neg = bsg[tr] < 0;
-          rs = row_ptr[r];
-          len = (int)(row_ptr[r + 1] - rs);
-        }
-        const int off = block_excl_scan_csr(len, wsum, &s_total);
-        // rows that fit entirely after `staged` entries (offsets grow with the
-        // thread index, so the fitting rows are a prefix of this round)
-        const bool fits = staged + off + len <= kStageCap;
-        const int nfit = __syncthreads_count(tr < end && fits);
-        if (tr < end && fits) {
-          for (int k = 0; k < len; ++k) {
-            s_col[staged + off + k] = col_idx[rs + k];
-            const double x = val[rs + k];
-            s_val[staged + off + k] = neg ? -x : x;
+      if (!whole) {
+        // ---- stage rows [rpos, ...) while they fit kStageCap nonzeros
+        staged = 0;
+        while (rnext < end) {
+          const int tr = rnext + (int)threadIdx.x;
+          int len = 0, neg = 0;
+          int64_t rs = 0;
+          if (tr < end) {
+            const int r = brow[tr];
+            neg = bsg[tr] < 0;
+            rs = row_ptr[r];
+            len = (int)(row_ptr[r + 1] - rs);
           }
-        }
-        int add = 0;
-        if (nfit > 0) {
-          // total staged entries of the fitting prefix = off + len of the last fitting row
-          __shared__ int s_last;
-          if (tr < end && fits && (threadIdx.x == nfit - 1)) s_last = off + len;
+          const int off = block_excl_scan_csr(len, wsum, &s_total);
+          // rows that fit after `staged` entries form a prefix of this round
+          const bool fits = tr < end && staged + off + len <= kStageCap;
+          const int nfit = __syncthreads_count(fits);
+          r_off[threadIdx.x] = staged + off;
+          r_start[threadIdx.x] = rs;
+          r_neg[threadIdx.x] = neg;
+          if (fits && (int)threadIdx.x == nfit - 1) r_off[nfit] = staged + off + len;
           __syncthreads();
-          add = s_last;
-        }
-        staged += add;
-        rnext += nfit;
-        __syncthreads();
-        if (nfit < kThreads || rnext >= end) {
-          if (nfit == 0 && staged == 0) {
-            // very long row (> kStageCap nonzeros): reduce it directly from global, chunk by chunk
-            const int r = brow[rnext];
-            const int neg = bsg[rnext] < 0;
-            const int64_t rs = row_ptr[r], re = row_ptr[r + 1];
-            for (int64_t q0 = rs; q0 < re; q0 += kStageCap) {
-              const int cnt = (int)min((int64_t)kStageCap, re - q0);
-              for (int k = threadIdx.x; k < cnt; k += kThreads) {
-                s_col[k] = col_idx[q0 + k];
-                const double x = val[q0 + k];
-                s_val[k] = neg ? -x : x;
+          if (nfit > 0) {
+            const int lo = staged, hi = r_off[nfit];
+            for (int e = lo + (int)threadIdx.x; e < hi; e += kThreads) {
+              int a = 0, z = nfit - 1;  // last row with r_off <= e
+              while (a < z) {
+                const int mid = (a + z + 1) >> 1;
+                if (r_off[mid] <= e) a = mid; else z = mid - 1;
               }
-              __syncthreads();
-              // columns within one row are distinct: no ordering among them
-              for (int k = threadIdx.x; k < cnt; k += kThreads) {
-                const int64_t cc = (int64_t)s_col[k] - c0;
-                if (cc >= 0 && cc < width) acc[cc] = acc[cc] + s_val[k];
-              }
-              __syncthreads();
+              const int64_t src = r_start[a] + (e - r_off[a]);
+              s_col[e] = col_idx[src];
+              const double x = val[src];
+              s_val[e] = r_neg[a] ? -x : x;
             }
-            rnext += 1;
+            staged = hi;
           }
-          break;
+          rnext += nfit;
+          __syncthreads();
+          if (nfit == 0 && staged == 0) {
+            // one row longer than the staging buffer: reduce it straight from
+            // global memory (its columns are distinct, so no ordering inside it)
+            const int r = brow[rnext];
+            const int ng = bsg[rnext] < 0;
+            const int64_t rs0 = row_ptr[r], re = row_ptr[r + 1];
+            for (int64_t q = rs0 + threadIdx.x; q < re; q += kThreads) {
+              const int64_t cc = (int64_t)col_idx[q] - c0;
+              if (cc >= 0 && cc < width) {
+                const double x = val[q];
+                acc[cc] = acc[cc] + (ng ? -x : x);
+              }
+            }
+            __syncthreads();
+            rnext += 1;
+            break;
+          }
+          if (nfit < kThreads || rnext >= end) break;
         }
+        if (rpos == beg && rnext >= end && staged > 0) whole = true;
+      } else {
+        rnext = end;
       }
       // ---- reduce the staged entries [0, staged) into the tile, canonical order
-      if (staged > 0) {
+      if (staged > 0 && (whole || rnext > rpos)) {
         const int cw = (width + kWarps - 1) / kWarps;
         const int clo = w * cw, chi = min(width, clo + cw);
         for (int e0 = 0; e0 < staged; e0 += 32) {
@@ -181,6 +187,7 @@ __global__ void __launch_bounds__(kThreads) gather_csr_kernel(
         }
       }
       __syncthreads();
+      if (!whole) staged = 0;
       rpos = rnext;
     }
     // ---- write the tile

@@ -33,6 +33,15 @@ constexpr int kGenThreads = 256;
 
 int wide_mode();
 
+}  // namespace
+
+// fwht_pipe.cu
+int launch_pipe_k(int K, bool diag, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo,
+                  int64_t d, int64_t g_begin, int64_t g_count, uint32_t* counters, uint64_t dkey, int64_t row0,
+                  double alpha, cudaStream_t st);
+
+namespace {
+
 __global__ void diag_words_kernel(uint64_t key, int64_t w0, int64_t nw, uint64_t* __restrict__ out) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q < nw) out[q] = stream_u(key, (uint64_t)(w0 + q));
@@ -114,14 +123,16 @@ __global__ void __launch_bounds__(tile_threads<K>()) fwht_tile_kernel(
   uint32_t negmask = 0;
   if (DIAG) {
     if (lo == 0) {
+      // 16 consecutive global rows g0..g0+15: their D bits are bits (g0 & 63) ..
+      // of the 128-bit word pair (wb:wa), one funnel shift
       const int64_t g0 = row0 + rbase + mid_of<K, 0>(rs, 0);
-      const uint64_t wa = stream_u(dkey, (uint64_t)(g0 >> 6)), wb = stream_u(dkey, (uint64_t)((g0 + 15) >> 6));
-#pragma unroll
-      for (int v = 0; v < 16; ++v) {
-        const int64_t gr = g0 + v;
-        const uint64_t w = ((gr >> 6) == (g0 >> 6)) ? wa : wb;
-        if (gr - row0 < nvalid) negmask |= (uint32_t)((w >> (gr & 63)) & 1ull) << v;
-      }
+      const uint64_t wa = stream_u(dkey, (uint64_t)(g0 >> 6));
+      const int sh = (int)(g0 & 63);
+      uint64_t win = wa >> sh;
+      if (sh > 48) win |= stream_u(dkey, (uint64_t)((g0 >> 6) + 1)) << (64 - sh);
+      const int64_t left = nvalid - (g0 - row0);
+      const uint32_t vmask = left >= 16 ? 0xFFFFu : (left <= 0 ? 0u : ((1u << left) - 1u));
+      negmask = (uint32_t)(win & 0xFFFFull) & vmask;
     } else {
 #pragma unroll
       for (int v = 0; v < 16; ++v) {
@@ -131,11 +142,21 @@ __global__ void __launch_bounds__(tile_threads<K>()) fwht_tile_kernel(
       }
     }
   }
+  // Phase-0 rows of this thread are r0 + v * 2^lo (v = 0..15): one base pointer
+  // and one stride instead of per-row 64-bit index arithmetic; rows >= nvalid
+  // (zero padding) are the tail v >= nv.
   double2 x[16];
+  {
+    const int64_t r0 = rbase + ((int64_t)(rs * 16) << lo);
+    const int64_t left = nvalid - r0;
+    const int nv = left <= 0 ? 0 : (left >= ((int64_t)16 << lo) ? 16 : (int)((left + ((int64_t)1 << lo) - 1) >> lo));
+    const double2* p = reinterpret_cast<const double2*>(X + r0 * ldx + c);
+    const int64_t step = (ldx << lo) / 2;  // in double2
 #pragma unroll
-  for (int v = 0; v < 16; ++v) {
-    const int64_t r = rbase + ((int64_t)mid_of<K, 0>(rs, v) << lo);
-    x[v] = (cv && r < nvalid) ? __ldg(reinterpret_cast<const double2*>(X + r * ldx + c)) : make_double2(0.0, 0.0);
+    for (int v = 0; v < 16; ++v) {
+      x[v] = make_double2(0.0, 0.0);
+      if (cv && v < nv) x[v] = __ldg(p + v * step);
+    }
   }
   if (DIAG) {
 #pragma unroll
@@ -152,10 +173,17 @@ __global__ void __launch_bounds__(tile_threads<K>()) fwht_tile_kernel(
     phase_stages<K, 2>(x);
   }
   if (cv) {
+    // last-phase mid = rs*NG + g + j*2^LB for v = g*J + j
+    constexpr int LB = 4 * (NPH - 1);
+    constexpr int BP = K - LB;
+    constexpr int J = 1 << BP;
+    constexpr int NG = 16 / J;
+    double2* q = reinterpret_cast<double2*>(Y + (rbase + ((int64_t)(rs * NG) << lo)) * ldy + c);
+    const int64_t sg = (ldy << lo) / 2, sj = (ldy << (lo + LB)) / 2;
 #pragma unroll
     for (int v = 0; v < 16; ++v) {
-      const int64_t r = rbase + ((int64_t)mid_of<K, NPH - 1>(rs, v) << lo);
-      *reinterpret_cast<double2*>(Y + r * ldy + c) = make_double2(alpha * x[v].x, alpha * x[v].y);
+      const int g2 = v / J, j = v % J;
+      q[g2 * sg + j * sj] = make_double2(alpha * x[v].x, alpha * x[v].y);
     }
   }
 }
@@ -283,7 +311,7 @@ __global__ void __launch_bounds__(tile_threads<KL>()) fwht_cluster_kernel(
 // A-tasks and tasks are claimed in dependency order, so the schedule cannot
 // deadlock whatever the residency.  Stage order stays low bit -> high bit.
 template <int KB, bool DIAG>
-__global__ void __launch_bounds__(256) fwht_fused_kernel(
+__global__ void __launch_bounds__(256, 3) fwht_fused_kernel(
     const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy, int64_t nvalid, int lo,
     int64_t d, int64_t ntc, int64_t g_begin, int64_t nunits, int64_t lag, uint32_t* __restrict__ counters,
     uint64_t dkey, int64_t row0, double alpha) {
@@ -372,9 +400,10 @@ __global__ void __launch_bounds__(256) fwht_fused_kernel(
           *reinterpret_cast<double2*>(Y + r * ldy + c) = x[v];
         }
       }
-      __threadfence();
+      // publish: CTA barrier, then one gpu-scope release (cumulative over the
+      // CTA's stores ordered before it by the barrier)
       __syncthreads();
-      if (threadIdx.x == 0) atomicAdd(done + u, 1u);
+      if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(done + u) : "memory");
     } else {
       if (threadIdx.x == 0) {
         unsigned ns = 32;
@@ -621,6 +650,8 @@ int launch_pass(bool fast, int K, const double* X, int64_t ldx, double* Y, int64
   if (fast) {
 #define SKH_TILE(KK) \
   case KK: return launch_tile_d<KK>(dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dkey, row0, alpha, st)
+    if (K >= 7 && K <= 11 && wide_mode() == 3)
+      return launch_pipe_k(K, dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0, alpha, st);
     if (K >= 9 && K <= 11 && wide_mode() == 1)
       return launch_fused_k(K, dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0, alpha, st);
     if (K >= 9 && K <= 11 && wide_mode() == 2)
@@ -668,15 +699,18 @@ int kmax_fast() {
   return v;
 }
 
-// Passes of 9..11 bits: 1 = fused through L2 (default), 2 = thread-block
-// clusters over DSMEM, 0 = single-CTA tiles (SKH_FWHT_WIDE = fused|cluster|tile).
+// Kernel for passes wider than 8 bits (only used when SKH_FWHT_KMAX > 8):
+// 0 = single-CTA tiles (default), 1 = fused through L2, 2 = thread-block
+// clusters over DSMEM, 3 = bulk-copy pipeline (also takes 7- and 8-bit passes);
+// SKH_FWHT_WIDE = tile|fused|cluster|pipe.  Measurements: DESIGN.md §5.
 int wide_mode() {
   static int v = [] {
     const char* e = getenv("SKH_FWHT_WIDE");
-    if (!e) return 1;
+    if (!e) return 0;
     if (e[0] == 'c') return 2;
-    if (e[0] == 't') return 0;
-    return 1;
+    if (e[0] == 'f') return 1;
+    if (e[0] == 'p') return 3;
+    return 0;  // "tile"
   }();
   return v;
 }
@@ -705,7 +739,7 @@ bool fwht_fast_ok(const double* X, int64_t ldx, const double* Y, int64_t ldy, in
 // Workspace of a transform call: [task counter + per-unit counters of fused
 // passes][D bitmap for the generic first pass].
 size_t fwht_counter_bytes(int64_t nrows, int64_t d) {
-  return align_up(sizeof(uint32_t) * (size_t)(64 + std::max<int64_t>(1, (nrows >> 9) * ((d + 63) / 64))));
+  return align_up(sizeof(uint32_t) * (size_t)(64 + std::max<int64_t>(1, (nrows >> 7) * ((d + 63) / 64))));
 }
 
 size_t fwht_ws_bytes(int64_t nrows, int64_t nvalid, int64_t row0, int64_t d) {

@@ -50,6 +50,19 @@ class CudaOps:
         return self.api.c_s(s)
 
 
+def all_to_all(out, inp, group=None):
+    """all_to_all_single with equal splits.  NCCL moves device tensors directly
+    (NVLink/NVSwitch); the gloo backend (CPU tests, single-GPU functional runs)
+    stages CUDA tensors through host memory."""
+    if inp.is_cuda and dist.get_backend(group) == "gloo":
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(o, inp.cpu(), group=group)
+        out.copy_(o)
+        return out
+    dist.all_to_all_single(out, inp, group=group)
+    return out
+
+
 def _log2(x):
     k = int(x).bit_length() - 1
     if (1 << k) != x:
@@ -102,38 +115,49 @@ class ShardedHrht:
         if isinstance(self.ops, CudaOps):
             self.ws = self.ops.api.rht_stages_workspace(self.L, self.L, self.r * self.L, d, A_loc.device)
 
-    def run(self):
+    STAGES = ("fwht_local", "all_to_all_rows", "fwht_cross", "hash_gen", "gather", "reduce")
+
+    def run(self, mark=None):
+        """One sharded step; ``mark(name)`` (optional) is called after each of
+        STAGES (bench.py records a CUDA event there)."""
+        mark = mark or (lambda name: None)
         ops, G, r, L = self.ops, self.G, self.r, self.L
         blk = L // G
         # R3 + R4 (local): global bits [0, log2 L) = local bits, D with global ids
         ops.rht_stages(self.seed, self.A, 0, self.lg, L, r * L, True, self.Y, self.ws)
         if self.b is not None:
             ops.rht_stages(self.seed, self.b.view(-1, 1), 0, self.lg, L, r * L, True, self.yb, self.ws)
+        mark("fwht_local")
         # R7: block q of rows [q*blk, (q+1)*blk) -> rank q (equal splits)
         if G > 1:
-            dist.all_to_all_single(self.Y2, self.Y, group=self.group)
+            all_to_all(self.Y2, self.Y, group=self.group)
             if self.b is not None:
-                dist.all_to_all_single(self.yb2, self.yb, group=self.group)
+                all_to_all(self.yb2, self.yb, group=self.group)
         else:
             self.Y2.copy_(self.Y)
             if self.b is not None:
                 self.yb2.copy_(self.yb)
+        mark("all_to_all_rows")
         # Y2 row k = g*blk + t holds global row g*L + r*blk + t; the rank bits g are
         # local bits [log2 blk, log2 L): the remaining global stages, low to high.
-        ops.rht_stages(self.seed, self.Y2, self.lq, self.lg, L, 0, False, self.Y2, self.ws)
-        if self.b is not None:
-            ops.rht_stages(self.seed, self.yb2, self.lq, self.lg, L, 0, False, self.yb2, self.ws)
+        if self.lq < self.lg:
+            ops.rht_stages(self.seed, self.Y2, self.lq, self.lg, L, 0, False, self.Y2, self.ws)
+            if self.b is not None:
+                ops.rht_stages(self.seed, self.yb2, self.lq, self.lg, L, 0, False, self.yb2, self.ws)
+        mark("fwht_cross")
         # R1 + R2 for exactly these global rows (ascending in k)
         self.bl = ops.hash_gen(self.seed, self.m, self.s, L, r * blk, blk, L, out=self.bl)
+        mark("hash_gen")
         # R5: unscaled partial sums of this rank's rows
         ops.sketch_dense(self.bl, self.Y2, None if self.b is None else self.yb2.view(-1), 1.0,
                          SA=self.P[: self.m], Sb=None if self.b is None else self.Pb[: self.m])
+        mark("gather")
         # R6 (M5): strips to their owners, then a rank-order sum scaled once by c_ns
         lo, hi = self.strips[r]
         if G > 1:
-            dist.all_to_all_single(self.R.view(G * self.mq, self.d), self.P, group=self.group)
+            all_to_all(self.R.view(G * self.mq, self.d), self.P, group=self.group)
             if self.b is not None:
-                dist.all_to_all_single(self.Rb.view(-1), self.Pb, group=self.group)
+                all_to_all(self.Rb.view(-1), self.Pb, group=self.group)
         else:
             self.R[0].copy_(self.P)
             if self.b is not None:
@@ -143,6 +167,7 @@ class ShardedHrht:
         if self.b is not None:
             ops.ordered_sum(self.Rb.view(G, self.mq, 1), self.alpha, out=self.outb)
             Sb = self.outb[: hi - lo, 0]
+        mark("reduce")
         return self.out[: hi - lo], Sb, (lo, hi)
 
 
@@ -174,16 +199,21 @@ class ShardedPlain:
         self.bl = None
         self.alpha = self.ops.c_s(self.s)
 
-    def run(self):
+    STAGES = ("hash_gen", "gather", "reduce")
+
+    def run(self, mark=None):
+        mark = mark or (lambda name: None)
         ops, G, r = self.ops, self.G, self.r
         self.bl = ops.hash_gen(self.seed, self.m, self.s, self.nloc, self.row0, 0, 0, out=self.bl)
+        mark("hash_gen")
         ops.sketch_dense(self.bl, self.A, self.b, 1.0, SA=self.P[: self.m],
                          Sb=None if self.b is None else self.Pb[: self.m])
+        mark("gather")
         lo, hi = self.strips[r]
         if G > 1:
-            dist.all_to_all_single(self.R.view(G * self.mq, self.d), self.P, group=self.group)
+            all_to_all(self.R.view(G * self.mq, self.d), self.P, group=self.group)
             if self.b is not None:
-                dist.all_to_all_single(self.Rb.view(-1), self.Pb, group=self.group)
+                all_to_all(self.Rb.view(-1), self.Pb, group=self.group)
         else:
             self.R[0].copy_(self.P)
             if self.b is not None:
@@ -193,7 +223,45 @@ class ShardedPlain:
         if self.b is not None:
             ops.ordered_sum(self.Rb.view(G, self.mq, 1), self.alpha, out=self.outb)
             Sb = self.outb[: hi - lo, 0]
+        mark("reduce")
         return self.out[: hi - lo], Sb, (lo, hi)
+
+
+class ShardedCsr:
+    """CSR A replicated on every rank (|SA| >> |A| for C4): rank r computes the
+    SA rows of its bucket strip, no collective; the strips
+    together are SA."""
+
+    def __init__(self, seed, row_ptr, col_idx, val, d, b, m, s, group=None):
+        from . import api
+        self.api = api
+        self.G = dist.get_world_size(group)
+        self.r = dist.get_rank(group)
+        self.seed, self.m, self.s, self.d = seed, int(m), int(s), int(d)
+        self.csr = (row_ptr, col_idx, val)
+        self.b = b
+        self.mq, self.strips = strip_rows(self.m, self.G)
+        lo, hi = self.strips[self.r]
+        dev = row_ptr.device
+        self.SA = torch.empty(max(hi - lo, 1), self.d, dtype=torch.float64, device=dev)
+        self.Sb = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=dev) if b is not None else None
+        self.bl = None
+
+    STAGES = ("hash_gen", "gather_csr")
+
+    def run(self, mark=None):
+        mark = mark or (lambda name: None)
+        api = self.api
+        n = self.csr[0].numel() - 1
+        self.bl = api.hash_gen(self.seed, self.m, self.s, n, out=self.bl)
+        mark("hash_gen")
+        lo, hi = self.strips[self.r]
+        if hi > lo:
+            strip = api.BucketLists(hi - lo, self.s, n, self.bl.ptr[lo:hi + 1], self.bl.rows, self.bl.signs)
+            api.sketch_csr(strip, *self.csr, self.d, self.b, SA=self.SA[: hi - lo],
+                           Sb=None if self.b is None else self.Sb[: hi - lo])
+        mark("gather_csr")
+        return self.SA[: hi - lo], None if self.b is None else self.Sb[: hi - lo], (lo, hi)
 
 
 def gather_strips(strip, lohi, m, group=None):
@@ -202,6 +270,8 @@ def gather_strips(strip, lohi, m, group=None):
     mq = math.ceil(m / G)
     buf = torch.zeros(mq, *strip.shape[1:], dtype=strip.dtype, device=strip.device)
     buf[: strip.shape[0]] = strip
+    if buf.is_cuda and dist.get_backend(group) == "gloo":
+        buf = buf.cpu()
     allb = [torch.empty_like(buf) for _ in range(G)]
     dist.all_gather(allb, buf, group=group)
-    return torch.cat(allb, 0)[:m]
+    return torch.cat(allb, 0)[:m].to(strip.device)

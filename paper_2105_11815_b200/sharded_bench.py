@@ -1,0 +1,173 @@
+"""bench.py's multi-GPU arm (torchrun, one process per GPU).
+
+Strong scaling of the BASELINE workload over N ranks (C5: "row-sharded over 8
+GPUs; runs at 1/2/4/8 GPUs"): rank r holds rows [r n/N, (r+1) n/N) of A and
+runs the sharded step of sharded.py (local FWHT passes, one all-to-all of rows,
+the cross stages, hash of its rows, gather, all-to-all of SA strips + rank-order
+sum).  Timed with CUDA events on every rank between barriers, reported as the
+max over ranks; rank 0 prints the JSON line.  The collectives use NCCL over
+NVLink/NVSwitch; SKH_DIST_BACKEND=gloo runs the same path functionally (host-
+staged collectives) for single-GPU smoke tests.
+"""
+import json
+import os
+import time
+
+
+def _stage_events(names, torch):
+    evs = {"start": torch.cuda.Event(enable_timing=True)}
+    for n in names:
+        evs[n] = torch.cuda.Event(enable_timing=True)
+    return evs
+
+
+def run(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from . import api, build, sharded
+    from synth import device
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("SKH_DIST_BACKEND", "nccl")
+    ndev = torch.cuda.device_count()
+    dev = local % max(ndev, 1)
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group(backend)
+    G = dist.get_world_size()
+    if rank == 0:
+        build.build()
+    dist.barrier()
+
+    def red_max(x):
+        t = torch.tensor([float(x)], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def red_sum(x):
+        t = torch.tensor([float(x)], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- inputs (this rank's shard) and the sharded step
+    if cfg.kind == "csr":
+        rp, ci, v = device.csr(cfg)
+        b = device.rhs(cfg)
+        step = sharded.ShardedCsr(cfg.seed, rp, ci, v, cfg.d, b, cfg.m, cfg.s)
+        shard = None
+    elif cfg.hd:
+        L = cfg.n // G
+        A = device.dense(cfg, rank * L, (rank + 1) * L)
+        b = device.rhs(cfg, rank * L, (rank + 1) * L)
+        step = sharded.ShardedHrht(cfg.seed, A, b, cfg.n, cfg.m, cfg.s)
+        shard = (A, b)
+    else:
+        per = (cfg.n + G - 1) // G
+        r0, r1 = min(cfg.n, rank * per), min(cfg.n, (rank + 1) * per)
+        A = device.dense(cfg, r0, r1)
+        b = device.rhs(cfg, r0, r1)
+        step = sharded.ShardedPlain(cfg.seed, A, b, cfg.n, cfg.m, cfg.s)
+        shard = (A, b)
+    torch.cuda.synchronize()
+    for _ in range(max(args.warmup, 0)):
+        step.run()
+    torch.cuda.synchronize()
+
+    # ---- timed region
+    names = list(step.STAGES)
+    evsets = [_stage_events(names, torch) for _ in range(args.steps)]
+    clk = None
+    if rank == 0:
+        from bench import ClockSampler
+        clk = ClockSampler(dev)
+        clk.start()
+        time.sleep(0.3)
+    n0 = api.launch_count()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(args.steps):
+        evs = evsets[k]
+        evs["start"].record()
+        step.run(mark=lambda nm, evs=evs: evs[nm].record())
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = red_sum(api.launch_count() - n0)
+    clocks = clk.stop() if clk else None
+    ms = red_max(e0.elapsed_time(e1)) / args.steps
+    stage_ms = {}
+    for nm in names:
+        tot = 0.0
+        for evs in evsets:
+            prev = "start" if nm == names[0] else names[names.index(nm) - 1]
+            tot += evs[prev].elapsed_time(evs[nm])
+        stage_ms[nm] = red_max(tot / len(evsets))
+
+    # ---- e2e: the same step fed from this rank's pinned host shard, strip read back
+    e2e = None
+    if shard is not None and not args.no_e2e:
+        A_d, b_d = shard
+        A_h = torch.empty(A_d.shape, dtype=torch.float64, pin_memory=True)
+        A_h.copy_(A_d)
+        b_h = torch.empty(b_d.shape, dtype=torch.float64, pin_memory=True)
+        b_h.copy_(b_d)
+        torch.cuda.synchronize()
+        t = []
+        out_bytes = 0
+        for _ in range(args.e2e_steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            A_d.copy_(A_h, non_blocking=True)
+            b_d.copy_(b_h, non_blocking=True)
+            SA, Sb, _ = step.run()
+            SA_h = SA.cpu()
+            Sb_h = Sb.cpu()
+            s1.record()
+            torch.cuda.synchronize()
+            out_bytes = SA_h.numel() * 8 + Sb_h.numel() * 8
+            t.append(s0.elapsed_time(s1))
+        ms_e2e = red_max(sum(t) / len(t))
+        e2e = {"value": cfg.a_bytes / (ms_e2e / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms_e2e,
+               "steps": args.e2e_steps, "h2d_bytes_per_step": int(red_sum(A_h.numel() * 8 + b_h.numel() * 8)),
+               "d2h_bytes_per_step": int(red_sum(out_bytes)), "api": type(step).__name__ + ".run (pinned shard)"}
+
+    if rank == 0:
+        from bench import METRIC, peaks
+        pk, src = peaks()
+        value = cfg.a_bytes / (ms / 1e3) / 1e9
+        line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": G, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "pct_hbm_peak": round(100 * value / (G * pk["hbm_gbs"]), 2),
+                "config": {"workload": cfg.name, "n": cfg.n, "d": cfg.d, "m": cfg.m, "s": cfg.s, "hd": cfg.hd,
+                           "a_bytes": cfg.a_bytes, "l2": "inputs (A) larger than L2; no flush",
+                           "parallelism": f"row-sharded x{G} ({type(step).__name__}, {backend})",
+                           "note": cfg.note},
+                "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+                "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e}
+        if cfg.hd:
+            L = cfg.n // G
+            npass = len(api.rht_pass_plan((L).bit_length() - 1, cfg.d))
+            alg = npass * 2 * L * cfg.d * 8
+            t = stage_ms["fwht_local"]
+            ach = alg / (t / 1e3) / 1e9
+            line["roofline"] = {"bound": "hbm", "kernel": f"fwht_tile_kernel ({npass} local passes, per rank)",
+                                "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                                "frac": round(ach / pk["hbm_gbs"], 4), "traffic": None, "peak_source": src}
+            a2a_bytes = (G - 1) * (L // G) * cfg.d * 8
+            ta = stage_ms["all_to_all_rows"]
+            line["comm"] = {"all_to_all_rows_bytes_sent_per_rank": a2a_bytes, "ms": round(ta, 4),
+                            "GBps_per_rank": round(a2a_bytes / (ta / 1e3) / 1e9, 1),
+                            "peer_peak_GBps": 770.0, "peak_source": "B200_PROFILING.md measured peer copy"}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
