@@ -5,16 +5,18 @@
 // One CTA per bucket (C4: m = 16384 buckets of ~192 rows x 8 nonzeros; SA is
 // 1 GiB dense, 91 % of the bytes -- the kernel is bound by writing SA once).
 //   Stage   256 rows per round, one per thread: row id + sign, then row_ptr, a
-//           block scan of the row lengths, then the nonzeros are copied in a
-//           flattened, coalesced loop (entry e finds its row by binary search
-//           in the scanned offsets) -- three dependent round trips per 256 rows,
-//           all loads of a round in flight together.  (column, signed value)
-//           pairs land in shared memory in list order.
-//   Reduce  per column tile (<= 4096 fp64 columns in shared memory, zero-filled
-//           in place): warp w owns 1/8 of the tile's columns and walks the
-//           staged list in order; lanes of one 32-entry step that hit the same
-//           column are combined by their lowest lane in lane order (= ascending
-//           row), so every column sees its terms in canonical order.
+//           block scan of the row lengths, then each thread copies its row's
+//           nonzeros (up to 16 loads in flight) -- three dependent round trips
+//           per 256 rows.  (column, signed value) pairs land in shared memory in
+//           list order.
+//   Bin     per column tile (<= 4096 fp64 columns in shared memory, zero-filled
+//           in place), a stable partition of the staged entries by owner warp
+//           (warp w owns a contiguous 1/8 of the tile) with warp ballots: warps
+//           take contiguous runs of 32-entry chunks, so order inside a bin is
+//           list order.
+//   Reduce  each warp walks its bin in order; lanes of one 32-entry step that
+//           hit the same column are combined by their lowest lane in lane order
+//           (= ascending row), so every column sees its terms in canonical order.
 //   Write   the tile is streamed out once with 16-byte stores.
 // A bucket whose nonzeros fit the staging buffer is staged once for all column
 // tiles; larger buckets are processed in row chunks, in order.
@@ -58,17 +60,18 @@ __device__ __forceinline__ int block_excl_scan_csr(int v, int* wsum, int* total)
   return r;
 }
 
-__global__ void __launch_bounds__(kThreads) gather_csr_kernel(
+__global__ void __launch_bounds__(kThreads, 3) gather_csr_kernel(
     int64_t m, const int32_t* __restrict__ ptr, const int32_t* __restrict__ brow, const int8_t* __restrict__ bsg,
     int64_t d, int tile_cols, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
     const double* __restrict__ val, double* __restrict__ SA, int64_t ldsa, double alpha) {
   extern __shared__ double acc[];  // [tile_cols]
   __shared__ int s_col[kStageCap];
   __shared__ double s_val[kStageCap];
-  __shared__ int r_off[kThreads + 1];  // staged offset of each row of the round (+ end)
-  __shared__ int64_t r_start[kThreads];
-  __shared__ int r_neg[kThreads];
+  __shared__ int16_t s_perm[kStageCap];
   __shared__ double stage[kWarps][32];
+  __shared__ int s_cnt[kWarps][kWarps];  // [bin][warp] entries of bin in warp's chunk run
+  __shared__ int s_bin[kWarps + 1];
+  __shared__ int s_end;
   __shared__ int wsum[32];
   __shared__ int s_total;
   const int64_t b = blockIdx.x;
@@ -81,6 +84,7 @@ __global__ void __launch_bounds__(kThreads) gather_csr_kernel(
 
   for (int t = 0; t < ntiles; ++t) {
     const int64_t c0 = (int64_t)t * tile_cols;
+    const int c0i = (int)c0;  // d < 2^31
     const int width = (int)min((int64_t)tile_cols, d - c0);
     for (int i = threadIdx.x; i < width; i += kThreads) acc[i] = 0.0;
     int rpos = beg;
@@ -103,28 +107,33 @@ __global__ void __launch_bounds__(kThreads) gather_csr_kernel(
           // rows that fit after `staged` entries form a prefix of this round
           const bool fits = tr < end && staged + off + len <= kStageCap;
           const int nfit = __syncthreads_count(fits);
-          r_off[threadIdx.x] = staged + off;
-          r_start[threadIdx.x] = rs;
-          r_neg[threadIdx.x] = neg;
-          if (fits && (int)threadIdx.x == nfit - 1) r_off[nfit] = staged + off + len;
-          __syncthreads();
-          if (nfit > 0) {
-            const int lo = staged, hi = r_off[nfit];
-            for (int e = lo + (int)threadIdx.x; e < hi; e += kThreads) {
-              int a = 0, z = nfit - 1;  // last row with r_off <= e
-              while (a < z) {
-                const int mid = (a + z + 1) >> 1;
-                if (r_off[mid] <= e) a = mid; else z = mid - 1;
+          if (fits && (int)threadIdx.x == nfit - 1) s_end = staged + off + len;
+          if (fits) {
+            // the first 16 nonzeros of the row are loaded together, then stored
+            const int o = staged + off;
+            int cbuf[16];
+            double vbuf[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+              if (k < len) {
+                cbuf[k] = col_idx[rs + k];
+                vbuf[k] = val[rs + k];
               }
-              const int64_t src = r_start[a] + (e - r_off[a]);
-              s_col[e] = col_idx[src];
-              const double x = val[src];
-              s_val[e] = r_neg[a] ? -x : x;
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+              if (k < len) {
+                s_col[o + k] = cbuf[k];
+                s_val[o + k] = neg ? -vbuf[k] : vbuf[k];
+              }
+            for (int k = 16; k < len; ++k) {
+              s_col[o + k] = col_idx[rs + k];
+              const double x = val[rs + k];
+              s_val[o + k] = neg ? -x : x;
             }
-            staged = hi;
           }
-          rnext += nfit;
           __syncthreads();
+          if (nfit > 0) staged = s_end;
+          rnext += nfit;
           if (nfit == 0 && staged == 0) {
             // one row longer than the staging buffer: reduce it straight from
             // global memory (its columns are distinct, so no ordering inside it)
@@ -132,8 +141,8 @@ __global__ void __launch_bounds__(kThreads) gather_csr_kernel(
             const int ng = bsg[rnext] < 0;
             const int64_t rs0 = row_ptr[r], re = row_ptr[r + 1];
             for (int64_t q = rs0 + threadIdx.x; q < re; q += kThreads) {
-              const int64_t cc = (int64_t)col_idx[q] - c0;
-              if (cc >= 0 && cc < width) {
+              const int cc = col_idx[q] - c0i;
+              if ((unsigned)cc < (unsigned)width) {
                 const double x = val[q];
                 acc[cc] = acc[cc] + (ng ? -x : x);
               }
@@ -149,41 +158,92 @@ __global__ void __launch_bounds__(kThreads) gather_csr_kernel(
         rnext = end;
       }
       // ---- reduce the staged entries [0, staged) into the tile, canonical order
-      if (staged > 0 && (whole || rnext > rpos)) {
-        const int cw = (width + kWarps - 1) / kWarps;
-        const int clo = w * cw, chi = min(width, clo + cw);
-        for (int e0 = 0; e0 < staged; e0 += 32) {
-          const int e = e0 + lane;
-          int col = -1;
-          double v = 0.0;
-          bool valid = false;
+      if (staged > 0) {
+        // warp w owns tile columns [w << cwl, (w+1) << cwl)
+        int cwl = 0;
+        while ((kWarps << cwl) < width) ++cwl;
+        const int nch = (staged + 31) >> 5;
+        const int cpw = (nch + kWarps - 1) / kWarps;
+        const int ch0 = min(nch, w * cpw), ch1 = min(nch, ch0 + cpw);
+        // pass 1: per-bin counts of this warp's chunk run
+        int cnt[kWarps];
+#pragma unroll
+        for (int q = 0; q < kWarps; ++q) cnt[q] = 0;
+        for (int ch = ch0; ch < ch1; ++ch) {
+          const int e = ch * 32 + lane;
+          int bn = kWarps;
           if (e < staged) {
-            const int64_t cc = (int64_t)s_col[e] - c0;
-            valid = cc >= clo && cc < chi;
-            if (valid) {
-              col = (int)cc;
-              v = s_val[e];
-            }
+            const int cc = s_col[e] - c0i;
+            if ((unsigned)cc < (unsigned)width) bn = cc >> cwl;
           }
-          const unsigned vm = __ballot_sync(0xffffffffu, valid);
-          if (vm) {
-            stage[w][lane] = v;
-            __syncwarp();
-            if (valid) {
-              const unsigned peers = __match_any_sync(vm, col);
-              if ((peers & lt) == 0) {
-                double a = acc[col];
-                unsigned pm = peers;
-                while (pm) {
-                  const int l = __ffs(pm) - 1;
-                  pm &= pm - 1;
-                  a = a + stage[w][l];
-                }
-                acc[col] = a;
-              }
+#pragma unroll
+          for (int q = 0; q < kWarps; ++q) cnt[q] += __popc(__ballot_sync(0xffffffffu, bn == q));
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int q = 0; q < kWarps; ++q) s_cnt[q][w] = cnt[q];
+        }
+        __syncthreads();
+        int pos[kWarps];
+        {
+          int run = 0;
+#pragma unroll
+          for (int q = 0; q < kWarps; ++q) {
+            if (threadIdx.x == 0) s_bin[q] = run;
+            int before = 0;
+            for (int x = 0; x < kWarps; ++x) {
+              const int v = s_cnt[q][x];
+              if (x < w) before += v;
+              run += v;
             }
-            __syncwarp();
+            pos[q] = before;  // + the bin start, added below
           }
+          if (threadIdx.x == 0) s_bin[kWarps] = run;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kWarps; ++q) pos[q] += s_bin[q];
+        // pass 2: write entry indices to their bins, in order
+        for (int ch = ch0; ch < ch1; ++ch) {
+          const int e = ch * 32 + lane;
+          int bn = kWarps;
+          if (e < staged) {
+            const int cc = s_col[e] - c0i;
+            if ((unsigned)cc < (unsigned)width) bn = cc >> cwl;
+          }
+#pragma unroll
+          for (int q = 0; q < kWarps; ++q) {
+            const unsigned mq = __ballot_sync(0xffffffffu, bn == q);
+            if (bn == q) s_perm[pos[q] + __popc(mq & lt)] = (int16_t)e;
+            pos[q] += __popc(mq);
+          }
+        }
+        __syncthreads();
+        const int b_lo = s_bin[w], b_hi = s_bin[w + 1];
+        for (int e0 = b_lo; e0 < b_hi; e0 += 32) {
+          const int ei = e0 + lane;
+          const bool valid = ei < b_hi;
+          int col = -1 - lane;  // distinct dummies keep the match convergent
+          double v = 0.0;
+          if (valid) {
+            const int e = s_perm[ei];
+            col = s_col[e] - c0i;
+            v = s_val[e];
+          }
+          stage[w][lane] = v;
+          const unsigned peers = __match_any_sync(0xffffffffu, col);
+          __syncwarp();
+          if (valid && (peers & lt) == 0) {  // leader = lowest lane = earliest row
+            double a = acc[col];
+            unsigned pm = peers;
+            while (pm) {
+              const int l = __ffs(pm) - 1;
+              pm &= pm - 1;
+              a = a + stage[w][l];
+            }
+            acc[col] = a;
+          }
+          __syncwarp();
         }
       }
       __syncthreads();

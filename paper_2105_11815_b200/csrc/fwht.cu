@@ -35,6 +35,10 @@ int wide_mode();
 
 }  // namespace
 
+// fwht_fused.cu
+int launch_fused2_k(int K, bool diag, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo,
+                    int64_t d, int64_t g_begin, int64_t g_count, uint32_t* counters, uint64_t dkey, int64_t row0,
+                    double alpha, cudaStream_t st);
 // fwht_pipe.cu
 int launch_pipe_k(int K, bool diag, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo,
                   int64_t d, int64_t g_begin, int64_t g_count, uint32_t* counters, uint64_t dkey, int64_t row0,
@@ -117,14 +121,29 @@ __global__ void __launch_bounds__(tile_threads<K>()) fwht_tile_kernel(
   const int64_t c = tc * TC + 2 * cp;
   const bool cv = c < d;
 
-  // D signs computed in registers from the splitmix64 words (no memory dependency
-  // ahead of the data loads).  Phase-0 rows of a thread are 16 consecutive rows
-  // when lo == 0, so two words cover them.
+  // Phase-0 rows of this thread are r0 + v * 2^lo (v = 0..15): one base pointer
+  // and one stride instead of per-row 64-bit index arithmetic; rows >= nvalid
+  // (zero padding) are the tail v >= nv.  The 16 loads are issued first; the D
+  // signs are computed while they are in flight.
+  double2 x[16];
+  {
+    const int64_t r0 = rbase + ((int64_t)(rs * 16) << lo);
+    const int64_t left = nvalid - r0;
+    const int nv = left <= 0 ? 0 : (left >= ((int64_t)16 << lo) ? 16 : (int)((left + ((int64_t)1 << lo) - 1) >> lo));
+    const double2* p = reinterpret_cast<const double2*>(X + r0 * ldx + c);
+    const int64_t step = (ldx << lo) / 2;  // in double2
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {
+      x[v] = make_double2(0.0, 0.0);
+      if (cv && v < nv) x[v] = __ldg(p + v * step);
+    }
+  }
+  // D signs from the splitmix64 words, in registers (no memory access).
   uint32_t negmask = 0;
   if (DIAG) {
     if (lo == 0) {
       // 16 consecutive global rows g0..g0+15: their D bits are bits (g0 & 63) ..
-      // of the 128-bit word pair (wb:wa), one funnel shift
+      // of the 128-bit word pair (w1:w0), one funnel shift
       const int64_t g0 = row0 + rbase + mid_of<K, 0>(rs, 0);
       const uint64_t wa = stream_u(dkey, (uint64_t)(g0 >> 6));
       const int sh = (int)(g0 & 63);
@@ -140,22 +159,6 @@ __global__ void __launch_bounds__(tile_threads<K>()) fwht_tile_kernel(
         const int64_t gr = row0 + r;
         if (r < nvalid) negmask |= (uint32_t)((stream_u(dkey, (uint64_t)(gr >> 6)) >> (gr & 63)) & 1ull) << v;
       }
-    }
-  }
-  // Phase-0 rows of this thread are r0 + v * 2^lo (v = 0..15): one base pointer
-  // and one stride instead of per-row 64-bit index arithmetic; rows >= nvalid
-  // (zero padding) are the tail v >= nv.
-  double2 x[16];
-  {
-    const int64_t r0 = rbase + ((int64_t)(rs * 16) << lo);
-    const int64_t left = nvalid - r0;
-    const int nv = left <= 0 ? 0 : (left >= ((int64_t)16 << lo) ? 16 : (int)((left + ((int64_t)1 << lo) - 1) >> lo));
-    const double2* p = reinterpret_cast<const double2*>(X + r0 * ldx + c);
-    const int64_t step = (ldx << lo) / 2;  // in double2
-#pragma unroll
-    for (int v = 0; v < 16; ++v) {
-      x[v] = make_double2(0.0, 0.0);
-      if (cv && v < nv) x[v] = __ldg(p + v * step);
     }
   }
   if (DIAG) {
@@ -652,6 +655,9 @@ int launch_pass(bool fast, int K, const double* X, int64_t ldx, double* Y, int64
   case KK: return launch_tile_d<KK>(dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dkey, row0, alpha, st)
     if (K >= 7 && K <= 11 && wide_mode() == 3)
       return launch_pipe_k(K, dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0, alpha, st);
+    if (K >= 8 && K <= 11 && wide_mode() == 4)
+      return launch_fused2_k(K, dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0, alpha,
+                             st);
     if (K >= 9 && K <= 11 && wide_mode() == 1)
       return launch_fused_k(K, dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0, alpha, st);
     if (K >= 9 && K <= 11 && wide_mode() == 2)
@@ -693,7 +699,7 @@ int kmax_fast() {
   // enables them for experiments.
   static int v = [] {
     const char* e = getenv("SKH_FWHT_KMAX");
-    int k = e ? atoi(e) : 8;
+    int k = e ? atoi(e) : 10;
     return k < 4 ? 4 : (k > 11 ? 11 : k);
   }();
   return v;
@@ -710,6 +716,7 @@ int wide_mode() {
     if (e[0] == 'c') return 2;
     if (e[0] == 'f') return 1;
     if (e[0] == 'p') return 3;
+    if (e[0] == 's') return 4;  // "sched": cooperative static-schedule fused passes
     return 0;  // "tile"
   }();
   return v;
@@ -726,8 +733,32 @@ std::vector<int> plan_passes(int L, bool fast) {
     return ks;
   }
   const int kmax = fast ? kmax_fast() : 5;
-  const int P = (L + kmax - 1) / kmax;
-  for (int p = 0; p < P; ++p) ks.push_back(L / P + (p < L % P ? 1 : 0));
+  if (!fast || kmax <= 8) {
+    const int P = (L + kmax - 1) / kmax;
+    for (int p = 0; p < P; ++p) ks.push_back(L / P + (p < L % P ? 1 : 0));
+    return ks;
+  }
+  // Wider tile passes read/write narrower row segments and run slower; pick the
+  // split of L bits minimising the summed relative pass cost (measured on B200,
+  // a 4..8-bit pass runs at the copy rate).
+  // (the small quadratic term prefers balanced splits among equal-cost ones)
+  auto cost = [](int K) {
+    return K <= 8 ? 1.0 + 0.001 * (K - 6) * (K - 6) : (K == 9 ? 1.28 : (K == 10 ? 2.2 : 2.4));
+  };
+  std::vector<double> best(L + 1, 1e30);
+  std::vector<int> pick(L + 1, 0);
+  best[0] = 0.0;
+  for (int l = 1; l <= L; ++l)
+    for (int K = 1; K <= std::min(l, kmax); ++K) {
+      if (K < 4 && l != K) continue;  // narrow passes only as the whole plan
+      const double c = best[l - K] + cost(K);
+      if (c < best[l] - 1e-9) {
+        best[l] = c;
+        pick[l] = K;
+      }
+    }
+  for (int l = L; l > 0; l -= pick[l]) ks.push_back(pick[l]);
+  std::sort(ks.begin(), ks.end(), [](int a, int b) { return a > b; });
   return ks;
 }
 
