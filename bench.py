@@ -133,7 +133,7 @@ def reference_arm(args, cfg):
     v = tot_b / tot_t / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "n": cfg.n, "d": cfg.d, "m": cfg.m, "s": cfg.s, "hd": cfg.hd,
                        "note": "CPU oracle on a bounded sample of the workload per step"},
             "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
@@ -255,7 +255,7 @@ def gpu_arm_single(args, cfg):
     pk, src = peaks()
     value = cfg.a_bytes / (ms / 1e3) / 1e9
     line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "pct_hbm_peak": round(100 * value / pk["hbm_gbs"], 2),
             "config": {"workload": cfg.name, "n": cfg.n, "d": cfg.d, "m": cfg.m, "s": cfg.s, "hd": cfg.hd,

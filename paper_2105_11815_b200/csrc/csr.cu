@@ -8,15 +8,15 @@
 //           block scan of the row lengths, then each thread copies its row's
 //           nonzeros (up to 16 loads in flight) -- three dependent round trips
 //           per 256 rows.  (column, signed value) pairs land in shared memory in
-//           list order.
-//   Bin     per column tile (<= 4096 fp64 columns in shared memory, zero-filled
-//           in place), a stable partition of the staged entries by owner warp
-//           (warp w owns a contiguous 1/8 of the tile) with warp ballots: warps
-//           take contiguous runs of 32-entry chunks, so order inside a bin is
-//           list order.
-//   Reduce  each warp walks its bin in order; lanes of one 32-entry step that
-//           hit the same column are combined by their lowest lane in lane order
-//           (= ascending row), so every column sees its terms in canonical order.
+//           list order (= ascending row; columns are distinct inside a row).
+//   Reduce  per column tile (<= 4096 fp64 columns in shared memory, zero-filled
+//           in place), the staged list is consumed 256 entries at a time, one per
+//           thread.  Entries of one chunk that share a column are applied in
+//           rounds: each pending entry claims its column with an integer
+//           atomicMin of its list index (order-free), the minimum adds its value,
+//           the rest retry -- so every column sees its terms in ascending list
+//           order, the canonical order.  Conflicts are rare (1536 entries over
+//           8192 columns), so a chunk takes ~2 rounds.
 //   Write   the tile is streamed out once with 16-byte stores.
 // A bucket whose nonzeros fit the staging buffer is staged once for all column
 // tiles; larger buckets are processed in row chunks, in order.
@@ -32,6 +32,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTileMax = 4096;   // fp64 accumulator columns per pass (32 KiB)
 constexpr int kStageCap = 2048;  // staged nonzeros (24 KiB)
+constexpr int kFree = 0x7fffffff;
 
 __device__ __forceinline__ int block_excl_scan_csr(int v, int* wsum, int* total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -67,16 +68,11 @@ __global__ void __launch_bounds__(kThreads, 3) gather_csr_kernel(
   extern __shared__ double acc[];  // [tile_cols]
   __shared__ int s_col[kStageCap];
   __shared__ double s_val[kStageCap];
-  __shared__ int16_t s_perm[kStageCap];
-  __shared__ double stage[kWarps][32];
-  __shared__ int s_cnt[kWarps][kWarps];  // [bin][warp] entries of bin in warp's chunk run
-  __shared__ int s_bin[kWarps + 1];
+  __shared__ int claim[kTileMax];
   __shared__ int s_end;
   __shared__ int wsum[32];
   __shared__ int s_total;
   const int64_t b = blockIdx.x;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
   const int beg = ptr[b], end = ptr[b + 1];
   const int ntiles = (int)((d + tile_cols - 1) / tile_cols);
   bool whole = false;  // the whole bucket sits in the staging buffer
@@ -86,7 +82,10 @@ __global__ void __launch_bounds__(kThreads, 3) gather_csr_kernel(
     const int64_t c0 = (int64_t)t * tile_cols;
     const int c0i = (int)c0;  // d < 2^31
     const int width = (int)min((int64_t)tile_cols, d - c0);
-    for (int i = threadIdx.x; i < width; i += kThreads) acc[i] = 0.0;
+    for (int i = threadIdx.x; i < width; i += kThreads) {
+      acc[i] = 0.0;
+      claim[i] = kFree;
+    }
     int rpos = beg;
     while (rpos < end) {
       int rnext = rpos;
@@ -158,92 +157,26 @@ __global__ void __launch_bounds__(kThreads, 3) gather_csr_kernel(
         rnext = end;
       }
       // ---- reduce the staged entries [0, staged) into the tile, canonical order
-      if (staged > 0) {
-        // warp w owns tile columns [w << cwl, (w+1) << cwl)
-        int cwl = 0;
-        while ((kWarps << cwl) < width) ++cwl;
-        const int nch = (staged + 31) >> 5;
-        const int cpw = (nch + kWarps - 1) / kWarps;
-        const int ch0 = min(nch, w * cpw), ch1 = min(nch, ch0 + cpw);
-        // pass 1: per-bin counts of this warp's chunk run
-        int cnt[kWarps];
-#pragma unroll
-        for (int q = 0; q < kWarps; ++q) cnt[q] = 0;
-        for (int ch = ch0; ch < ch1; ++ch) {
-          const int e = ch * 32 + lane;
-          int bn = kWarps;
-          if (e < staged) {
-            const int cc = s_col[e] - c0i;
-            if ((unsigned)cc < (unsigned)width) bn = cc >> cwl;
-          }
-#pragma unroll
-          for (int q = 0; q < kWarps; ++q) cnt[q] += __popc(__ballot_sync(0xffffffffu, bn == q));
+      for (int e0 = 0; e0 < staged; e0 += kThreads) {
+        const int e = e0 + (int)threadIdx.x;
+        int col = 0;
+        double v = 0.0;
+        bool pending = false;
+        if (e < staged) {
+          col = s_col[e] - c0i;
+          pending = (unsigned)col < (unsigned)width;
+          if (pending) v = s_val[e];
         }
-        if (lane == 0) {
-#pragma unroll
-          for (int q = 0; q < kWarps; ++q) s_cnt[q][w] = cnt[q];
-        }
-        __syncthreads();
-        int pos[kWarps];
-        {
-          int run = 0;
-#pragma unroll
-          for (int q = 0; q < kWarps; ++q) {
-            if (threadIdx.x == 0) s_bin[q] = run;
-            int before = 0;
-            for (int x = 0; x < kWarps; ++x) {
-              const int v = s_cnt[q][x];
-              if (x < w) before += v;
-              run += v;
-            }
-            pos[q] = before;  // + the bin start, added below
+        while (__syncthreads_or(pending)) {
+          if (pending) atomicMin(&claim[col], e);
+          __syncthreads();
+          const bool win = pending && claim[col] == e;
+          __syncthreads();
+          if (win) {  // the earliest pending entry of this column in the chunk
+            acc[col] = acc[col] + v;
+            claim[col] = kFree;
+            pending = false;
           }
-          if (threadIdx.x == 0) s_bin[kWarps] = run;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < kWarps; ++q) pos[q] += s_bin[q];
-        // pass 2: write entry indices to their bins, in order
-        for (int ch = ch0; ch < ch1; ++ch) {
-          const int e = ch * 32 + lane;
-          int bn = kWarps;
-          if (e < staged) {
-            const int cc = s_col[e] - c0i;
-            if ((unsigned)cc < (unsigned)width) bn = cc >> cwl;
-          }
-#pragma unroll
-          for (int q = 0; q < kWarps; ++q) {
-            const unsigned mq = __ballot_sync(0xffffffffu, bn == q);
-            if (bn == q) s_perm[pos[q] + __popc(mq & lt)] = (int16_t)e;
-            pos[q] += __popc(mq);
-          }
-        }
-        __syncthreads();
-        const int b_lo = s_bin[w], b_hi = s_bin[w + 1];
-        for (int e0 = b_lo; e0 < b_hi; e0 += 32) {
-          const int ei = e0 + lane;
-          const bool valid = ei < b_hi;
-          int col = -1 - lane;  // distinct dummies keep the match convergent
-          double v = 0.0;
-          if (valid) {
-            const int e = s_perm[ei];
-            col = s_col[e] - c0i;
-            v = s_val[e];
-          }
-          stage[w][lane] = v;
-          const unsigned peers = __match_any_sync(0xffffffffu, col);
-          __syncwarp();
-          if (valid && (peers & lt) == 0) {  // leader = lowest lane = earliest row
-            double a = acc[col];
-            unsigned pm = peers;
-            while (pm) {
-              const int l = __ffs(pm) - 1;
-              pm &= pm - 1;
-              a = a + stage[w][l];
-            }
-            acc[col] = a;
-          }
-          __syncwarp();
         }
       }
       __syncthreads();
