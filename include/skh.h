@@ -139,15 +139,22 @@ int skh_sketch_dense(int64_t m, int32_t s,
  * R5, sparse: SA (dense m x d) and Sb for A in CSR form, same
  * summation order as skh_sketch_dense applied to the rows of A.
  *   row_ptr [nrows+1] int64, col_idx [nnz] int32 (distinct within a row, each
- *   < d), val [nnz] f64.  Column indices need not be sorted.
+ *   < d), val [nnz] f64, nnz = row_ptr[nrows] (passed by the caller, so the
+ *   library needs no device read).  Column indices need not be sorted.
+ *   The bucket lists must be complete lists over all nrows rows (each row in
+ *   exactly s buckets); bucket_ptr may be an offset view of m consecutive
+ *   buckets of them (a bucket strip).  ws: skh_sketch_csr_workspace_bytes
+ *   (the expanded (column, value) list of S.A, 12 * s * nnz bytes + 8 * nrows * s).
+ *   Errors: SKH_EOVERFLOW if s * nnz >= 2^31.
  * ------------------------------------------------------------------------ */
+size_t skh_sketch_csr_workspace_bytes(int64_t nrows, int32_t s, int64_t nnz);
 int skh_sketch_csr(int64_t m, int32_t s,
                    const int32_t* bucket_ptr, const int32_t* bucket_rows,
                    const int8_t* bucket_signs,
-                   int64_t nrows, int64_t d, const int64_t* row_ptr,
+                   int64_t nrows, int64_t d, int64_t nnz, const int64_t* row_ptr,
                    const int32_t* col_idx, const double* val,
                    const double* b, double* SA, int64_t ldsa, double* Sb,
-                   double alpha, void* stream);
+                   double alpha, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ *
  * R3 + R4: Y = alpha * Hhat_[bit_lo,bit_hi) (D?) X along the row index.

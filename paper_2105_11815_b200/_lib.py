@@ -27,8 +27,9 @@ SIGNATURES = {
     "skh_hash_status": (ctypes.c_int, [c_p, c_p]),
     "skh_sketch_dense": (ctypes.c_int, [c_i64, c_i32, c_p, c_p, c_p, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_i64, c_p,
                                         c_d, c_p]),
-    "skh_sketch_csr": (ctypes.c_int, [c_i64, c_i32, c_p, c_p, c_p, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_i64, c_p,
-                                      c_d, c_p]),
+    "skh_sketch_csr_workspace_bytes": (c_sz, [c_i64, c_i32, c_i64]),
+    "skh_sketch_csr": (ctypes.c_int, [c_i64, c_i32, c_p, c_p, c_p, c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_i64,
+                                      c_p, c_d, c_p, c_sz, c_p]),
     "skh_rht_stages_workspace_bytes": (c_sz, [c_i64, c_i64, c_i64, c_i64]),
     "skh_rht_pass_plan": (ctypes.c_int, [ctypes.c_int, c_i64, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                          ctypes.c_int]),

@@ -111,19 +111,29 @@ def sketch_dense(bl, A, b=None, alpha=None, SA=None, Sb=None):
     return SA, Sb
 
 
-def sketch_csr(bl, row_ptr, col_idx, val, d, b=None, alpha=None, SA=None, Sb=None):
-    """R5 sparse (CSR A): dense SA = alpha * S A."""
+def sketch_csr_workspace(nrows, s, nnz, device=None):
+    lib = _lib.load()
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    return _workspace(lib.skh_sketch_csr_workspace_bytes(int(nrows), int(s), int(nnz)), device)
+
+
+def sketch_csr(bl, row_ptr, col_idx, val, d, b=None, alpha=None, SA=None, Sb=None, ws=None):
+    """R5 sparse (CSR A): dense SA = alpha * S A (nnz = len(val))."""
     lib = _lib.load()
     _need_cuda(row_ptr, col_idx, val, b)
     n = row_ptr.numel() - 1
+    nnz = val.numel()
     dev = row_ptr.device
     if SA is None:
         SA = torch.empty(bl.m, d, dtype=torch.float64, device=dev)
     if b is not None and Sb is None:
         Sb = torch.empty(bl.m, dtype=torch.float64, device=dev)
+    if ws is None:
+        ws = sketch_csr_workspace(n, bl.s, nnz, dev)
     alpha = c_s(bl.s) if alpha is None else float(alpha)
-    rc = lib.skh_sketch_csr(bl.m, bl.s, _ptr(bl.ptr), _ptr(bl.rows), _ptr(bl.signs), n, int(d), _ptr(row_ptr),
-                            _ptr(col_idx), _ptr(val), _ptr(b), _ptr(SA), _ld(SA), _ptr(Sb), alpha, _stream())
+    rc = lib.skh_sketch_csr(bl.m, bl.s, _ptr(bl.ptr), _ptr(bl.rows), _ptr(bl.signs), n, int(d), nnz, _ptr(row_ptr),
+                            _ptr(col_idx), _ptr(val), _ptr(b), _ptr(SA), _ld(SA), _ptr(Sb), alpha, _ptr(ws),
+                            ws.numel(), _stream())
     _lib.check(rc, "skh_sketch_csr")
     return SA, Sb
 

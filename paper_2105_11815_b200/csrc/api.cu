@@ -287,22 +287,37 @@ int skh_sketch_dense(int64_t m, int32_t s, const int32_t* bucket_ptr, const int3
   return rc;
 }
 
+size_t skh_sketch_csr_workspace_bytes(int64_t nrows, int32_t s, int64_t nnz) {
+  if (nrows < 0 || s < 1 || nnz < 0) return 0;
+  return csr_ws_bytes(nrows, s, nnz);
+}
+
 int skh_sketch_csr(int64_t m, int32_t s, const int32_t* bucket_ptr, const int32_t* bucket_rows,
-                   const int8_t* bucket_signs, int64_t nrows, int64_t d, const int64_t* row_ptr,
+                   const int8_t* bucket_signs, int64_t nrows, int64_t d, int64_t nnz, const int64_t* row_ptr,
                    const int32_t* col_idx, const double* val, const double* b, double* SA, int64_t ldsa, double* Sb,
-                   double alpha, void* stream) {
+                   double alpha, void* ws, size_t ws_bytes, void* stream) {
   int rc = validate_hash_args(m, s, nrows);
   if (rc) return rc;
-  if (d < 1 || !bucket_ptr || !SA || (nrows > 0 && (!row_ptr || !bucket_rows || !bucket_signs))) {
-    set_error("sketch_csr: d >= 1 and non-NULL bucket lists, row_ptr, SA required");
+  if (d < 1 || nnz < 0 || !bucket_ptr || !SA || (nrows > 0 && (!row_ptr || !bucket_rows || !bucket_signs)) ||
+      (nnz > 0 && (!col_idx || !val))) {
+    set_error("sketch_csr: d >= 1, nnz >= 0 and non-NULL bucket lists, row_ptr, col_idx, val, SA required");
     return SKH_EINVAL;
   }
   if (d >= (1ll << 31) || ldsa < d || (b && !Sb)) {
     set_error("sketch_csr: ldsa < d, d too large, or Sb NULL with b given");
     return SKH_EDIM;
   }
+  if (nnz * (int64_t)s >= (1ll << 31)) {
+    set_error("sketch_csr: s * nnz exceeds int32 offsets");
+    return SKH_EOVERFLOW;
+  }
+  if (!ws || ws_bytes < csr_ws_bytes(nrows, s, nnz)) {
+    set_error("sketch_csr workspace too small: need %zu bytes", csr_ws_bytes(nrows, s, nnz));
+    return SKH_EWORKSPACE;
+  }
   cudaStream_t st = as_stream(stream);
-  rc = launch_gather_csr(m, bucket_ptr, bucket_rows, bucket_signs, d, row_ptr, col_idx, val, SA, ldsa, alpha, st);
+  rc = launch_gather_csr(m, s, bucket_ptr, bucket_rows, bucket_signs, nrows, d, nnz, row_ptr, col_idx, val, SA, ldsa,
+                         alpha, ws, st);
   if (rc) return rc;
   if (b) rc = launch_gather_vec(m, bucket_ptr, bucket_rows, bucket_signs, b, Sb, alpha, st);
   return rc;

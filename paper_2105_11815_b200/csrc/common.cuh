@@ -55,6 +55,8 @@ int launch_hash(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, in
                 int32_t* bucket_rows, int8_t* bucket_signs, void* ws, size_t ws_bytes,
                 cudaStream_t st);
 int hash_status(const void* ws, cudaStream_t st);
+int64_t scan_scratch_ints(int64_t len);
+int launch_excl_scan_i32(int32_t* a, int64_t len, int32_t* blocksums, cudaStream_t st);
 // gather.cu
 int launch_gather_dense(int64_t m, const int32_t* ptr, const int32_t* rows, const int8_t* sg,
                         int64_t d, const double* A, int64_t lda, double* SA, int64_t ldsa,
@@ -62,9 +64,10 @@ int launch_gather_dense(int64_t m, const int32_t* ptr, const int32_t* rows, cons
 int launch_gather_vec(int64_t m, const int32_t* ptr, const int32_t* rows, const int8_t* sg,
                       const double* b, double* Sb, double alpha, cudaStream_t st);
 // csr.cu
-int launch_gather_csr(int64_t m, const int32_t* ptr, const int32_t* rows, const int8_t* sg,
-                      int64_t d, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
-                      double* SA, int64_t ldsa, double alpha, cudaStream_t st);
+size_t csr_ws_bytes(int64_t nrows, int s, int64_t nnz);
+int launch_gather_csr(int64_t m, int s, const int32_t* ptr, const int32_t* rows, const int8_t* sg,
+                      int64_t nrows, int64_t d, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                      const double* val, double* SA, int64_t ldsa, double alpha, void* ws, cudaStream_t st);
 // fwht.cu
 size_t fwht_ws_bytes(int64_t nrows, int64_t nvalid, int64_t row0, int64_t d);
 int launch_fwht(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, int64_t d,

@@ -97,31 +97,27 @@ __global__ void __launch_bounds__(kWarps * 32) gather_dense_kernel(
   }
 }
 
-// Sb: one thread per bucket, sequential over its list with kU loads in flight.
+// Sb: one warp per bucket.  32 entries are loaded at once (one per lane), then
+// added to the running sum in list order by lane 0 via shuffles -- the same
+// sequential order as the oracle.
 __global__ void gather_vec_kernel(int64_t m, const int32_t* __restrict__ ptr, const int32_t* __restrict__ rows,
                                   const int8_t* __restrict__ sg, const double* __restrict__ x,
                                   double* __restrict__ out, double alpha) {
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (b >= m) return;
   const int beg = ptr[b], end = ptr[b + 1];
   double acc = 0.0;
-  for (int t0 = beg; t0 < end; t0 += kU) {
-    double v[kU];
-    int ng[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      v[u] = 0.0;
-      ng[u] = 0;
-      if (t0 + u < end) {
-        v[u] = __ldg(x + rows[t0 + u]);
-        ng[u] = sg[t0 + u] < 0;
-      }
+  for (int t0 = beg; t0 < end; t0 += 32) {
+    const int cnt = min(32, end - t0);
+    double v = 0.0;
+    if (lane < cnt) {
+      v = __ldg(x + rows[t0 + lane]);
+      if (sg[t0 + lane] < 0) v = -v;
     }
-#pragma unroll
-    for (int u = 0; u < kU; ++u)
-      if (t0 + u < end) acc = ng[u] ? acc - v[u] : acc + v[u];
+    for (int u = 0; u < cnt; ++u) acc = acc + __shfl_sync(0xffffffffu, v, u);
   }
-  out[b] = alpha * acc;
+  if (lane == 0) out[b] = alpha * acc;
 }
 
 }  // namespace
@@ -149,7 +145,8 @@ int launch_gather_dense(int64_t m, const int32_t* ptr, const int32_t* rows, cons
 
 int launch_gather_vec(int64_t m, const int32_t* ptr, const int32_t* rows, const int8_t* sg, const double* b,
                       double* Sb, double alpha, cudaStream_t st) {
-  gather_vec_kernel<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(m, ptr, rows, sg, b, Sb, alpha); note_launch();
+  gather_vec_kernel<<<(unsigned)((m * 32 + 127) / 128), 128, 0, st>>>(m, ptr, rows, sg, b, Sb, alpha);
+  note_launch();
   return check_launch("gather_vec");
 }
 

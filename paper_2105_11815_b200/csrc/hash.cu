@@ -458,6 +458,12 @@ int launch_hash_seg(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0
 
 }  // namespace
 
+// Exclusive scan of int32 a[0..len) in place; blocksums needs scan_scratch_ints(len).
+int64_t scan_scratch_ints(int64_t len) { return scan_blocks(len) + 1; }
+int launch_excl_scan_i32(int32_t* a, int64_t len, int32_t* blocksums, cudaStream_t st) {
+  return excl_scan(a, len, blocksums, st);
+}
+
 size_t hash_ws_bytes(int64_t nrows, int64_t m, int s) {
   const int64_t N = nrows * (int64_t)s;
   const int64_t nt = ntiles_of(N);

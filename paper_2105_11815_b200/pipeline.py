@@ -132,6 +132,7 @@ class CsrStep:
         self.SA = torch.empty(self.m, self.d, dtype=torch.float64, device=dev)
         self.Sb = torch.empty(self.m, dtype=torch.float64, device=dev) if b is not None else None
         self.bl = None
+        self.ws = api.sketch_csr_workspace(row_ptr.numel() - 1, s, val.numel(), dev)
         self.timer = _Timed(["hash_gen", "gather_csr"], record)
 
     def new_timer(self):
@@ -143,6 +144,6 @@ class CsrStep:
         n = self.csr[0].numel() - 1
         self.bl = api.hash_gen(self.seed, self.m, self.s, n, out=self.bl)
         t.mark()
-        api.sketch_csr(self.bl, *self.csr, self.d, self.b, SA=self.SA, Sb=self.Sb)
+        api.sketch_csr(self.bl, *self.csr, self.d, self.b, SA=self.SA, Sb=self.Sb, ws=self.ws)
         t.mark()
         return self.SA, self.Sb

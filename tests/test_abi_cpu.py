@@ -58,7 +58,10 @@ def test_error_codes(lib):
     assert lib.skh_sketch_dense(8, 2, p, p, p, 10, 4, p, 3, None, p, 4, None, 1.0, None) == EDIM
     assert lib.skh_sketch_dense(8, 2, p, p, p, 10, 4, p, 4, p, p, 4, None, 1.0, None) == EDIM
     assert lib.skh_sketch_dense(8, 9, p, p, p, 10, 4, p, 4, None, p, 4, None, 1.0, None) == EINVAL
-    assert lib.skh_sketch_csr(8, 2, p, p, p, 10, 4, p, p, p, None, p, 3, None, 1.0, None) == EDIM
+    assert lib.skh_sketch_csr(8, 2, p, p, p, 10, 4, 80, p, p, p, None, p, 3, None, 1.0, p, 1 << 30, None) == EDIM
+    assert lib.skh_sketch_csr(8, 2, p, p, p, 10, 4, 80, p, p, p, None, p, 4, None, 1.0, p, 16, None) == EWS
+    assert lib.skh_sketch_csr(8, 2, p, p, p, 10, 4, 1 << 30, p, p, p, None, p, 4, None, 1.0, p, 1 << 40,
+                              None) == EOVERFLOW
     # rht_stages: nrows not a multiple of 2^bit_hi; in place with padding
     assert lib.skh_rht_stages(1, 12, 12, 0, 4, p, 4, p, 4, 0, 3, 0, 1.0, None, 0, None) == ENOTPOW2
     assert lib.skh_rht_stages(1, 16, 12, 0, 4, p, 4, p, 4, 0, 4, 0, 1.0, None, 0, None) == EDIM

@@ -32,6 +32,14 @@ if "fused" in which or "tile" in which or "gather" in which:
             skh.sketch_dense(bl, Y, alpha=1.0)
     torch.cuda.synchronize()
     del A, Y
+if "gather2" in which:  # C3: s = 2, 64-column slices re-read through L2
+    cfg = configs.C3
+    A = device.dense(cfg)
+    bl = skh.hash_gen(cfg.seed, cfg.m, cfg.s, cfg.n)
+    for rep in range(2):
+        skh.sketch_dense(bl, A)
+    torch.cuda.synchronize()
+    del A
 if "csr" in which:
     cfg = configs.C4
     rp, ci, v = device.csr(cfg)
