@@ -110,8 +110,8 @@ def oracle_sample(cfg, ncols):
 def cpu_baseline(cfg, target_s=12.0):
     ncols = 1
     nbytes, t, what = oracle_sample(cfg, ncols)
-    if t < target_s / 4 and cfg.kind != "csr":
-        ncols = max(1, min(cfg.d, int(ncols * target_s / max(t, 1e-3) / 2)))
+    if t < target_s / 2 and cfg.kind != "csr":
+        ncols = max(1, min(cfg.d, int(ncols * target_s / max(t, 1e-3))))
         nbytes, t, what = oracle_sample(cfg, ncols)
     return {"value": nbytes / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
             "sample": f"{what}; {t:.2f} s single-threaded NumPy", "seconds": round(t, 3)}
