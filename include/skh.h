@@ -228,6 +228,70 @@ int skh_ordered_sum(const double* parts, int64_t G, int64_t part_stride,
                     int64_t rows, int64_t cols, int64_t ldp,
                     double* out, int64_t ldo, double alpha, void* stream);
 
+/* ======================================================================== *
+ * Column-major A (the paper's own LAPACK/FFTW storage, L1073-1081): column c
+ * of A is A[c*lda .. c*lda + n), lda >= n; SA is column-major m x d,
+ * SA[c*ldsa + bucket], ldsa >= m.  Restrictions: s <= 8, m <= 65536.
+ * ======================================================================== */
+
+/* R1-R5: SA = S_h H D A, Sb = S_h H D b (Def. def::HRHT, L790-801), n padded
+ * to n_pad = 2^L with zero rows.  Two HBM passes: D and the butterflies of
+ * row bits 0..12 on contiguous 2^13-row chunks, then the bits 13..L-1 on
+ * 2^(L-13)-row groups fused with the sketch (the transformed rows are never
+ * written back; each SA column accumulates in on-chip memory).  Bits beyond 21
+ * take extra in-place passes of <= 8 bits before the fused one.
+ * Summation order (R17): a bucket receives the rows of each 4096-row
+ * gather tile in ascending order, tile after tile -- fixed, so the result is
+ * bitwise reproducible, but not the oracle's order: SA agrees with the oracle
+ * to rounding (relative Frobenius 1e-12) and exactly on integer data.
+ *   A [n x d] col-major (lda >= n), b [n] nullable, SA [m x d] col-major
+ *   (ldsa >= m), Sb [m] (required iff b).  ws: the workspace query (it holds
+ *   the transformed copy of A, (d + 1) * n_pad doubles). */
+size_t skh_rht_dense_colmajor_workspace_bytes(int64_t n, int64_t m, int32_t s, int64_t d);
+int skh_rht_dense_colmajor(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d,
+                           const double* A, int64_t lda, const double* b,
+                           double* SA, int64_t ldsa, double* Sb,
+                           void* ws, size_t ws_bytes, void* stream);
+/* Same from HOST buffers (pinned recommended): A_host is copied in groups of
+ * columns on a library copy stream, each group transformed (pass 1) as soon as
+ * it lands; SA_host/Sb_host receive the result.  Synchronise `stream` before
+ * reading them.  Workspace: skh_rht_dense_colmajor_workspace_bytes. */
+int skh_rht_dense_colmajor_host(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d,
+                                const double* A_host, int64_t lda, const double* b_host,
+                                double* SA_host, int64_t ldsa, double* Sb_host,
+                                void* ws, size_t ws_bytes, void* stream);
+
+/* R1, R2, R5: plain s-hashing SA = S A, Sb = S b of a column-major A (one HBM
+ * read of A).  Gather tiles are consecutive 4096-row blocks, so every bucket
+ * sums its rows in ascending order from +0.0 and scales once by c_s: the
+ * result is bit-identical to skh_sketch_dense and to the oracle. */
+size_t skh_sketch_dense_colmajor_workspace_bytes(int64_t n, int64_t m, int32_t s);
+int skh_sketch_dense_colmajor(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d,
+                              const double* A, int64_t lda, const double* b,
+                              double* SA, int64_t ldsa, double* Sb,
+                              void* ws, size_t ws_bytes, void* stream);
+
+/* R3 + R4 on column-major data: Y = Hhat D? X along the row index of every
+ * column, unnormalised, all log2(nrows) stages low bit to high bit (bit-exact
+ * with the oracle's radix-2 order).  nrows = 2^L (else SKH_ENOTPOW2); rows
+ * >= nvalid of X read as zero; D uses global rows row0 + i.  Y may alias X
+ * when nvalid == nrows.  X [ncols][ldx >= nvalid], Y [ncols][ldy >= nrows]. */
+int skh_rht_colmajor(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, int64_t ncols,
+                     const double* X, int64_t ldx, double* Y, int64_t ldy, int apply_diag,
+                     void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * Stage trace (thread-local).  After skh_trace_set(events, n) with n
+ * caller-created cudaEvent_t handles (as void*), every composite entry point
+ * (skh_*_colmajor*) records events[0] on its stream when it starts and
+ * events[i] after stage i, up to n events; skh_trace_count() returns the number
+ * recorded by the last call and skh_trace_name(i) the stage that events[i]
+ * closes ("begin" for 0).  skh_trace_set(NULL, 0) disables tracing.
+ * ------------------------------------------------------------------------ */
+int skh_trace_set(void* const* events, int nevents);
+int skh_trace_count(void);
+const char* skh_trace_name(int i);
+
 #ifdef __cplusplus
 }
 #endif

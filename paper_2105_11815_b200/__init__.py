@@ -4,5 +4,6 @@ The product is libskh.so (CUDA kernels for sm_100a behind the C ABI in
 include/skh.h); this package is its thin Python binding (``api``) plus the
 multi-GPU sequencing (``sharded``).  See DESIGN.md.
 """
-from .api import (BucketLists, RhtDense, SketchDenseHost, c_n, c_ns, c_s, hash_gen, hash_status,  # noqa: F401
-                  ordered_sum, rht_dense, rht_stages, scale, sketch_csr, sketch_dense)
+from .api import (BucketLists, RhtDense, RhtDenseColMajor, SketchDenseHost, Trace, c_n, c_ns, c_s,  # noqa: F401
+                  hash_gen, hash_status, ordered_sum, rht_colmajor, rht_dense, rht_dense_colmajor, rht_stages,
+                  scale, sketch_csr, sketch_dense, sketch_dense_colmajor)

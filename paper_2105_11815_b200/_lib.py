@@ -45,6 +45,19 @@ SIGNATURES = {
                                              c_sz, c_p]),
     "skh_scale": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_d, c_p]),
     "skh_ordered_sum": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_p, c_i64, c_d, c_p]),
+    "skh_rht_dense_colmajor_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32, c_i64]),
+    "skh_rht_dense_colmajor": (ctypes.c_int, [c_u64, c_i64, c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_p, c_i64, c_p,
+                                              c_p, c_sz, c_p]),
+    "skh_rht_dense_colmajor_host": (ctypes.c_int, [c_u64, c_i64, c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_p, c_i64,
+                                                   c_p, c_p, c_sz, c_p]),
+    "skh_sketch_dense_colmajor_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32]),
+    "skh_sketch_dense_colmajor": (ctypes.c_int, [c_u64, c_i64, c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_p, c_i64, c_p,
+                                                 c_p, c_sz, c_p]),
+    "skh_rht_colmajor": (ctypes.c_int, [c_u64, c_i64, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_i64, ctypes.c_int,
+                                        c_p]),
+    "skh_trace_set": (ctypes.c_int, [ctypes.POINTER(c_p), ctypes.c_int]),
+    "skh_trace_count": (ctypes.c_int, []),
+    "skh_trace_name": (ctypes.c_char_p, [ctypes.c_int]),
 }
 
 _lib = None

@@ -266,3 +266,127 @@ def ordered_sum(parts, alpha=1.0, out=None):
                              float(alpha), _stream())
     _lib.check(rc, "skh_ordered_sum")
     return out
+
+
+# ---------------------------------------------------------------- column-major A
+# The paper's own storage (LAPACK/FFTW, L1073-1081).  A torch tensor ``At`` of
+# shape (d, n) with unit last stride IS a column-major n x d matrix with
+# lda = At.stride(0); SA comes back the same way, as a (d, m) tensor = SA^T.
+
+def _ld_cm(t, rows):
+    if t.dim() != 2 or t.stride(1) != 1 or t.stride(0) < rows:
+        raise ValueError("expected a (cols, rows) tensor with unit last stride (column-major storage)")
+    return t.stride(0)
+
+
+class RhtDenseColMajor:
+    """SA = S_h H D A for column-major A (skh_rht_dense_colmajor): two HBM passes,
+    the second fused with the sketch.  Returns SA^T (d, m) and Sb."""
+
+    def __init__(self, n, m, s, d, device=None):
+        lib = _lib.load()
+        self.n, self.m, self.s, self.d = int(n), int(m), int(s), int(d)
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        self.ws = _workspace(lib.skh_rht_dense_colmajor_workspace_bytes(n, m, s, d), device)
+
+    def __call__(self, seed, At, b=None, SAt=None, Sb=None):
+        lib = _lib.load()
+        _need_cuda(At, b)
+        if tuple(At.shape) != (self.d, self.n) or At.dtype != torch.float64:
+            raise ValueError(f"At must be float64 of shape (d, n) = ({self.d}, {self.n})")
+        if SAt is None:
+            SAt = torch.empty(self.d, self.m, dtype=torch.float64, device=At.device)
+        if b is not None and Sb is None:
+            Sb = torch.empty(self.m, dtype=torch.float64, device=At.device)
+        rc = lib.skh_rht_dense_colmajor(int(seed) & (2**64 - 1), self.n, self.m, self.s, self.d, _ptr(At),
+                                        _ld_cm(At, self.n), _ptr(b), _ptr(SAt), _ld_cm(SAt, self.m), _ptr(Sb),
+                                        _ptr(self.ws), self.ws.numel(), _stream())
+        _lib.check(rc, "skh_rht_dense_colmajor")
+        return SAt, Sb
+
+    def from_host(self, seed, At_host, b_host=None, SAt_host=None, Sb_host=None):
+        """Same from host (pinned) tensors; returns host SA^T, Sb after syncing the stream."""
+        lib = _lib.load()
+        if At_host.is_cuda:
+            raise ValueError("from_host takes CPU tensors")
+        if SAt_host is None:
+            SAt_host = torch.empty(self.d, self.m, dtype=torch.float64, pin_memory=True)
+        if b_host is not None and Sb_host is None:
+            Sb_host = torch.empty(self.m, dtype=torch.float64, pin_memory=True)
+        rc = lib.skh_rht_dense_colmajor_host(int(seed) & (2**64 - 1), self.n, self.m, self.s, self.d,
+                                             _ptr(At_host), _ld_cm(At_host, self.n), _ptr(b_host), _ptr(SAt_host),
+                                             _ld_cm(SAt_host, self.m), _ptr(Sb_host), _ptr(self.ws),
+                                             self.ws.numel(), _stream())
+        _lib.check(rc, "skh_rht_dense_colmajor_host")
+        torch.cuda.current_stream().synchronize()
+        return SAt_host, Sb_host
+
+
+def rht_dense_colmajor(seed, At, b, m, s):
+    """SA^T, Sb for column-major A given as At (d, n)."""
+    d, n = At.shape
+    return RhtDenseColMajor(n, m, s, d, At.device)(seed, At, b)
+
+
+def sketch_dense_colmajor(seed, At, b, m, s, SAt=None, Sb=None, ws=None):
+    """Plain s-hashing SA = S A of column-major A (At: (d, n)); bit-identical to sketch_dense."""
+    lib = _lib.load()
+    _need_cuda(At, b)
+    d, n = At.shape
+    if SAt is None:
+        SAt = torch.empty(d, m, dtype=torch.float64, device=At.device)
+    if b is not None and Sb is None:
+        Sb = torch.empty(m, dtype=torch.float64, device=At.device)
+    if ws is None:
+        ws = _workspace(lib.skh_sketch_dense_colmajor_workspace_bytes(n, m, s), At.device)
+    rc = lib.skh_sketch_dense_colmajor(int(seed) & (2**64 - 1), n, int(m), int(s), d, _ptr(At), _ld_cm(At, n),
+                                       _ptr(b), _ptr(SAt), _ld_cm(SAt, m), _ptr(Sb), _ptr(ws), ws.numel(), _stream())
+    _lib.check(rc, "skh_sketch_dense_colmajor")
+    return SAt, Sb
+
+
+def rht_colmajor(seed, Xt, nrows=None, row0=0, apply_diag=True, Yt=None):
+    """Yt = (Hhat D? X)^T for column-major X given as Xt (ncols, nvalid): unnormalised, all stages."""
+    lib = _lib.load()
+    _need_cuda(Xt)
+    if Xt.dim() == 1:
+        Xt = Xt.view(1, -1)
+    ncols, nvalid = Xt.shape
+    nrows = nvalid if nrows is None else int(nrows)
+    if Yt is None:
+        Yt = torch.empty(ncols, nrows, dtype=torch.float64, device=Xt.device)
+    rc = lib.skh_rht_colmajor(int(seed) & (2**64 - 1), nrows, nvalid, int(row0), ncols, _ptr(Xt),
+                              max(Xt.stride(0), nvalid), _ptr(Yt), max(Yt.stride(0), nrows), int(bool(apply_diag)),
+                              _stream())
+    _lib.check(rc, "skh_rht_colmajor")
+    return Yt
+
+
+class Trace:
+    """Per-stage CUDA events recorded by the library's composite calls (skh_trace_set)."""
+
+    def __init__(self, n=16):
+        import ctypes
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+        for e in self.events:  # torch creates the CUDA event lazily
+            e.record()
+        torch.cuda.synchronize()
+        self._arr = (ctypes.c_void_p * n)(*[e.cuda_event for e in self.events])
+
+    def __enter__(self):
+        _lib.check(_lib.load().skh_trace_set(self._arr, len(self.events)), "skh_trace_set")
+        return self
+
+    def __exit__(self, *exc):
+        lib = _lib.load()
+        self.count = lib.skh_trace_count()
+        self.names = [lib.skh_trace_name(i).decode() for i in range(self.count)]
+        lib.skh_trace_set(None, 0)
+        return False
+
+    def durations_ms(self):
+        """{stage: ms} of the last traced call (synchronize first)."""
+        out = {}
+        for i in range(1, self.count):
+            out[self.names[i]] = out.get(self.names[i], 0.0) + self.events[i - 1].elapsed_time(self.events[i])
+        return out

@@ -204,6 +204,9 @@ int rht_tail(uint64_t seed, int64_t n, int64_t n_pad, int L, int64_t m, int s, i
 }
 
 }  // namespace
+
+cudaStream_t skh_copy_stream() { return copy_stream(); }
+
 }  // namespace skh
 
 using namespace skh;

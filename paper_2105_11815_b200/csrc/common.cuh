@@ -76,6 +76,12 @@ int launch_fwht(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, int6
 // util (api.cu)
 int launch_scale(double* X, int64_t rows, int64_t cols, int64_t ldx, double alpha, cudaStream_t st);
 
+// api_cm.cu: stage trace (skh_trace_set) -- records the caller's event after a stage
+void skh_trace_mark(cudaStream_t st, const char* name);
+void skh_trace_start(cudaStream_t st);
+// api.cu: library-owned copy stream of the current device (host-buffer variants)
+cudaStream_t skh_copy_stream();
+
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 }  // namespace skh

@@ -55,6 +55,25 @@ __global__ void dense_kernel(int kind, uint64_t seed, int64_t n_total, int64_t d
   }
 }
 
+// Same values, column-major: out[c * ld + i] (i fastest, coalesced writes).
+__global__ void dense_cm_kernel(int kind, uint64_t seed, int64_t n_total, int64_t d, int64_t row0, int64_t nrows,
+                                double* __restrict__ out, int64_t ld) {
+  const uint64_t ka = stream_key(seed, LABEL_A), ku = stream_key(seed, LABEL_DIAGU);
+  const int64_t total = nrows * d;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / nrows, i = e % nrows, gi = row0 + i;
+    double v = normal_at(ka, (uint64_t)(gi * d + c));
+    if (kind == 1) {
+      v = __dmul_rn(1e-8, v);
+      if (gi == c && gi < (n_total < d ? n_total : d)) {
+        const double dv = __dadd_rn(1.0, __dmul_rn(9.0, uniform01_at(ku, (uint64_t)gi)));
+        v = __dadd_rn(dv, v);
+      }
+    }
+    out[c * ld + i] = v;
+  }
+}
+
 __global__ void rhs_kernel(uint64_t seed, int64_t row0, int64_t n, double* __restrict__ out) {
   const uint64_t kb = stream_key(seed, LABEL_B);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -121,6 +140,14 @@ int synth_dense(int kind, uint64_t seed, int64_t n_total, int64_t d, int64_t row
                 int64_t ld, void* stream) {
   if (nrows <= 0) return 0;
   dense_kernel<<<grid_for(nrows * d), 256, 0, (cudaStream_t)stream>>>(kind, seed, n_total, d, row0, nrows, out, ld);
+  return cudaGetLastError() == cudaSuccess ? 0 : 7;
+}
+
+int synth_dense_cm(int kind, uint64_t seed, int64_t n_total, int64_t d, int64_t row0, int64_t nrows, double* out,
+                   int64_t ld, void* stream) {
+  if (nrows <= 0) return 0;
+  dense_cm_kernel<<<grid_for(nrows * d), 256, 0, (cudaStream_t)stream>>>(kind, seed, n_total, d, row0, nrows, out,
+                                                                          ld);
   return cudaGetLastError() == cudaSuccess ? 0 : 7;
 }
 

@@ -19,6 +19,7 @@ def load():
         lib = ctypes.CDLL(p)
         i64, u64, vp = ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p
         lib.synth_dense.argtypes = [ctypes.c_int, u64, i64, i64, i64, i64, vp, i64, vp]
+        lib.synth_dense_cm.argtypes = [ctypes.c_int, u64, i64, i64, i64, i64, vp, i64, vp]
         lib.synth_rhs.argtypes = [u64, i64, i64, vp, vp]
         lib.synth_csr.argtypes = [u64, i64, ctypes.c_int, i64, i64, vp, vp, vp, vp, vp]
         lib.synth_small_int.argtypes = [u64, i64, i64, ctypes.c_int, ctypes.c_int, vp, vp]
@@ -38,6 +39,19 @@ def dense(cfg, r0=0, r1=None, out=None, device="cuda"):
     rc = load().synth_dense(KIND[cfg.kind], cfg.seed, cfg.n, cfg.d, r0, r1 - r0, out.data_ptr(), out.stride(0), _st())
     if rc:
         raise RuntimeError("synth_dense failed")
+    return out
+
+
+def dense_colmajor(cfg, r0=0, r1=None, out=None, device="cuda"):
+    """Rows [r0, r1) of the config's dense A stored column-major: a (d, r1 - r0)
+    tensor At with At[c, i] = A[r0 + i, c] (same values as dense())."""
+    r1 = cfg.n if r1 is None else r1
+    if out is None:
+        out = torch.empty(cfg.d, r1 - r0, dtype=torch.float64, device=device)
+    rc = load().synth_dense_cm(KIND[cfg.kind], cfg.seed, cfg.n, cfg.d, r0, r1 - r0, out.data_ptr(), out.stride(0),
+                               _st())
+    if rc:
+        raise RuntimeError("synth_dense_cm failed")
     return out
 
 
