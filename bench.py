@@ -2,7 +2,8 @@
 """Benchmark of the hashing-sketch hot path (BASELINE.json metric:
 "sketch GB/s of A streamed (S.A, S.H.D.A) & % HBM peak at 1/2/4/8 B200").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5] [--layout row|col]
+                    [--impl reference]
 
 A step is one pass of the whole hot path over the workload (SURVEY §8(a) rows
 R1-R5; R6/R7 as well when N > 1): hash_gen (draw S_h, bucket lists), the D +
@@ -146,9 +147,13 @@ METRIC = "sketch GB/s of A streamed (S.A, S.H.D.A) & % HBM peak"
 
 
 # ---------------------------------------------------------------- GPU arm, one GPU
-def build_step(cfg, torch):
+def build_step(cfg, torch, layout="row"):
     from paper_2105_11815_b200 import pipeline
     from synth import device
+    if layout == "col" and cfg.kind != "csr":
+        At = device.dense_colmajor(cfg)
+        b = device.rhs(cfg)
+        return pipeline.ColStep(cfg.seed, At, b, cfg.m, cfg.s, cfg.hd, record=True), (At, b)
     if cfg.kind == "csr":
         rp, ci, v = device.csr(cfg)
         b = device.rhs(cfg)
@@ -159,11 +164,11 @@ def build_step(cfg, torch):
     return cls(cfg.seed, A, b, cfg.m, cfg.s, record=True), (A, b)
 
 
-def e2e_measure(cfg, inputs, steps, torch):
+def e2e_measure(cfg, inputs, steps, torch, layout="row"):
     """Same metric through the host-buffer C-ABI call: H2D of A and b and D2H of
     SA and Sb inside the timed region (pinned host buffers)."""
     import paper_2105_11815_b200 as skh
-    if cfg.kind == "csr":
+    if cfg.kind == "csr" or (layout == "col" and not cfg.hd):
         return None
     A, b = inputs
     A_h = torch.empty(A.shape, dtype=torch.float64, pin_memory=True)
@@ -171,13 +176,18 @@ def e2e_measure(cfg, inputs, steps, torch):
     b_h = torch.empty(b.shape, dtype=torch.float64, pin_memory=True)
     b_h.copy_(b)
     torch.cuda.synchronize()
-    if cfg.hd:
+    if layout == "col":
+        op = skh.RhtDenseColMajor(cfg.n, cfg.m, cfg.s, cfg.d)
+        call = op.from_host
+    elif cfg.hd:
         op = skh.RhtDense(cfg.n, cfg.m, cfg.s, cfg.d)
         call = op.from_host
     else:
         op = skh.SketchDenseHost(cfg.n, cfg.m, cfg.s, cfg.d)
         call = op
     SA_h = torch.empty(cfg.m, cfg.d, dtype=torch.float64, pin_memory=True)
+    if layout == "col":
+        SA_h = torch.empty(cfg.d, cfg.m, dtype=torch.float64, pin_memory=True)
     Sb_h = torch.empty(cfg.m, dtype=torch.float64, pin_memory=True)
     call(cfg.seed, A_h, b_h, SA_h, Sb_h)  # warm-up
     t = []
@@ -193,11 +203,28 @@ def e2e_measure(cfg, inputs, steps, torch):
     ms = sum(t) / len(t)
     return {"value": cfg.a_bytes / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms, "steps": steps,
             "h2d_bytes_per_step": A.numel() * 8 + b.numel() * 8, "d2h_bytes_per_step": cfg.m * cfg.d * 8 + cfg.m * 8,
-            "api": "skh_rht_dense_host" if cfg.hd else "skh_sketch_dense_host"}
+            "api": ("skh_rht_dense_colmajor_host" if layout == "col" else
+                    "skh_rht_dense_host" if cfg.hd else "skh_sketch_dense_host")}
 
 
-def roofline(cfg, step, stage_ms, peak_gbs, peak_src):
+def roofline(cfg, step, stage_ms, peak_gbs, peak_src, layout="row"):
     """Dominant kernel and its algorithmic bytes per launch."""
+    if layout == "col":
+        # dominant by time; algorithmic bytes of each kernel per launch:
+        #  pass1: read + write (d + 1) columns of n_pad rows once
+        #  pass2_gather / gather: read the columns once, write SA, read the tile lists
+        cols = cfg.d + 1
+        nrows = step.n_pad if cfg.hd else cfg.n
+        lists = nrows * cfg.s * 4
+        alg = {"pass1": 2 * step.n_pad * cols * 8,
+               "pass2_gather": nrows * cols * 8 + cfg.m * cols * 8 + lists,
+               "gather": nrows * cols * 8 + cfg.m * cols * 8 + lists}
+        name = max((k for k in stage_ms if k in alg), key=lambda k: stage_ms[k])
+        t = stage_ms[name]
+        achieved = alg[name] / (t / 1e3) / 1e9
+        return {"bound": "hbm", "kernel": "cm_" + name, "achieved": round(achieved, 1), "peak": peak_gbs,
+                "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": None, "traffic_source": None,
+                "alg_bytes_per_launch": alg[name], "ms_per_launch": round(t, 4), "peak_source": peak_src}
     if cfg.kind == "csr":
         name = "gather_csr"
         nnz = cfg.n * cfg.nnz_row
@@ -230,7 +257,7 @@ def gpu_arm_single(args, cfg):
 
     import paper_2105_11815_b200 as skh
     torch.cuda.set_device(0)
-    step, inputs = build_step(cfg, torch)
+    step, inputs = build_step(cfg, torch, args.layout)
     torch.cuda.synchronize()
     for _ in range(max(args.warmup, 0)):
         step.run()
@@ -259,14 +286,15 @@ def gpu_arm_single(args, cfg):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "pct_hbm_peak": round(100 * value / pk["hbm_gbs"], 2),
             "config": {"workload": cfg.name, "n": cfg.n, "d": cfg.d, "m": cfg.m, "s": cfg.s, "hd": cfg.hd,
-                       "a_bytes": cfg.a_bytes, "l2": "inputs (A) larger than L2; no flush",
+                       "a_bytes": cfg.a_bytes, "layout": "column-major" if args.layout == "col" else "row-major",
+                       "l2": "inputs (A) larger than L2; no flush",
                        "parallelism": "single GPU", "note": cfg.note},
             "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
             "gpu_launches": int(launches), "clocks": clocks}
-    line["roofline"] = roofline(cfg, step, stage_ms, pk["hbm_gbs"], src)
+    line["roofline"] = roofline(cfg, step, stage_ms, pk["hbm_gbs"], src, args.layout)
     del step
     if not args.no_e2e:
-        line["e2e"] = e2e_measure(cfg, inputs, args.e2e_steps, torch)
+        line["e2e"] = e2e_measure(cfg, inputs, args.e2e_steps, torch, args.layout)
     del inputs
     torch.cuda.empty_cache()
     if not args.no_cpu_baseline:
@@ -280,6 +308,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="C5")
+    ap.add_argument("--layout", default="row", choices=["row", "col"],
+                    help="storage of dense A: row-major (default) or column-major (the paper's LAPACK layout)")
     ap.add_argument("--impl", default="skh", choices=["skh", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
@@ -291,6 +321,8 @@ def main():
         return reference_arm(args, cfg)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
+        if args.layout == "col":
+            raise SystemExit("--layout col is single-GPU in this build (sharded runs use row-major A)")
         from paper_2105_11815_b200 import sharded_bench
         return sharded_bench.run(args, cfg)
     from paper_2105_11815_b200 import build

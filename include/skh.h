@@ -113,6 +113,21 @@ int skh_hash_gen(uint64_t seed, int64_t m, int32_t s,
                  int32_t* col_rows, int8_t* col_signs,
                  int32_t* bucket_ptr, int32_t* bucket_rows, int8_t* bucket_signs,
                  void* ws, size_t ws_bytes, void* stream);
+/* The s-hashing VARIANT T (Def. def::s-hashing-variant, L683-686: "sample
+ * with replacement i_1..i_s in [m] uniformly at random and add +-1/sqrt(s) to
+ * T_{i_k j}"; Lemma 8: T = s^{-1/2} (S^(1) + ... + S^(s)) for
+ * independent 1-hashings).  Same arguments, outputs and workspace as
+ * skh_hash_gen; draw k = 0..s-1 of column j is r_k = floor(u(key, j*2^16 + k)
+ * * m / 2^64) with NO rejection (so with s = 1 it equals skh_hash_gen), sign bit
+ * k of the sign word.  A row drawn twice for one column appears twice in that
+ * bucket (adjacent, + before -; R18); every consumer of bucket lists
+ * (skh_sketch_dense, skh_sketch_csr, ...) then computes T A, T b.  Never
+ * reports SKH_ERETRY. */
+int skh_hash_gen_variant(uint64_t seed, int64_t m, int32_t s,
+                         int64_t nrows, int64_t row0, int64_t blk, int64_t stride,
+                         int32_t* col_rows, int8_t* col_signs,
+                         int32_t* bucket_ptr, int32_t* bucket_rows, int8_t* bucket_signs,
+                         void* ws, size_t ws_bytes, void* stream);
 /* Synchronises `stream` and returns SKH_OK or SKH_ERETRY for the last
  * skh_hash_gen that used workspace `ws`. */
 int skh_hash_status(const void* ws, void* stream);

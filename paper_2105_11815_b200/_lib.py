@@ -24,6 +24,8 @@ SIGNATURES = {
     "skh_hash_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32]),
     "skh_hash_gen": (ctypes.c_int, [c_u64, c_i64, c_i32, c_i64, c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p, c_p,
                                     c_sz, c_p]),
+    "skh_hash_gen_variant": (ctypes.c_int, [c_u64, c_i64, c_i32, c_i64, c_i64, c_i64, c_i64, c_p, c_p, c_p, c_p, c_p,
+                                            c_p, c_sz, c_p]),
     "skh_hash_status": (ctypes.c_int, [c_p, c_p]),
     "skh_sketch_dense": (ctypes.c_int, [c_i64, c_i32, c_p, c_p, c_p, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_i64, c_p,
                                         c_d, c_p]),

@@ -67,8 +67,9 @@ class BucketLists:
     ws: torch.Tensor = None
 
 
-def hash_gen(seed, m, s, nrows, row0=0, blk=0, stride=0, want_cols=False, device=None, out=None):
-    """R1+R2: draw the s-hashing columns j(k) and build bucket lists."""
+def hash_gen(seed, m, s, nrows, row0=0, blk=0, stride=0, want_cols=False, device=None, out=None, variant=False):
+    """R1+R2: draw the s-hashing columns j(k) and build bucket lists
+    (variant=True: the s-hashing variant of Def. 7, draws with replacement)."""
     lib = _lib.load()
     device = device or torch.device("cuda", torch.cuda.current_device())
     N = int(nrows) * int(s)
@@ -81,10 +82,11 @@ def hash_gen(seed, m, s, nrows, row0=0, blk=0, stride=0, want_cols=False, device
             out.col_rows = torch.empty(max(N, 1), dtype=torch.int32, device=device)
             out.col_signs = torch.empty(max(N, 1), dtype=torch.int8, device=device)
         out.ws = _workspace(lib.skh_hash_workspace_bytes(nrows, m, s), device)
-    rc = lib.skh_hash_gen(int(seed) & (2**64 - 1), int(m), int(s), int(nrows), int(row0), int(blk), int(stride),
-                          _ptr(out.col_rows), _ptr(out.col_signs), _ptr(out.ptr), _ptr(out.rows), _ptr(out.signs),
-                          _ptr(out.ws), out.ws.numel(), _stream())
-    _lib.check(rc, "skh_hash_gen")
+    fn = lib.skh_hash_gen_variant if variant else lib.skh_hash_gen
+    rc = fn(int(seed) & (2**64 - 1), int(m), int(s), int(nrows), int(row0), int(blk), int(stride),
+            _ptr(out.col_rows), _ptr(out.col_signs), _ptr(out.ptr), _ptr(out.rows), _ptr(out.signs),
+            _ptr(out.ws), out.ws.numel(), _stream())
+    _lib.check(rc, "skh_hash_gen_variant" if variant else "skh_hash_gen")
     return out
 
 

@@ -240,9 +240,10 @@ size_t skh_hash_workspace_bytes(int64_t nrows, int64_t m, int32_t s) {
   return hash_ws_bytes(nrows, m, s);
 }
 
-int skh_hash_gen(uint64_t seed, int64_t m, int32_t s, int64_t nrows, int64_t row0, int64_t blk, int64_t stride,
-                 int32_t* col_rows, int8_t* col_signs, int32_t* bucket_ptr, int32_t* bucket_rows,
-                 int8_t* bucket_signs, void* ws, size_t ws_bytes, void* stream) {
+static int hash_gen_impl(uint64_t seed, int64_t m, int32_t s, int64_t nrows, int64_t row0, int64_t blk,
+                         int64_t stride, int32_t* col_rows, int8_t* col_signs, int32_t* bucket_ptr,
+                         int32_t* bucket_rows, int8_t* bucket_signs, void* ws, size_t ws_bytes, int variant,
+                         void* stream) {
   int rc = validate_hash_args(m, s, nrows);
   if (rc) return rc;
   if (!bucket_ptr || (nrows > 0 && (!bucket_rows || !bucket_signs))) {
@@ -261,8 +262,22 @@ int skh_hash_gen(uint64_t seed, int64_t m, int32_t s, int64_t nrows, int64_t row
     set_error("hash workspace too small: need %zu bytes", hash_ws_bytes(nrows, m, s));
     return SKH_EWORKSPACE;
   }
-  return launch_hash(seed, m, s, nrows, row0, blk, stride, col_rows, col_signs, bucket_ptr, bucket_rows, bucket_signs,
-                     ws, ws_bytes, as_stream(stream));
+  return launch_hash_v(seed, m, s, nrows, row0, blk, stride, col_rows, col_signs, bucket_ptr, bucket_rows,
+                       bucket_signs, ws, ws_bytes, variant, as_stream(stream));
+}
+
+int skh_hash_gen(uint64_t seed, int64_t m, int32_t s, int64_t nrows, int64_t row0, int64_t blk, int64_t stride,
+                 int32_t* col_rows, int8_t* col_signs, int32_t* bucket_ptr, int32_t* bucket_rows,
+                 int8_t* bucket_signs, void* ws, size_t ws_bytes, void* stream) {
+  return hash_gen_impl(seed, m, s, nrows, row0, blk, stride, col_rows, col_signs, bucket_ptr, bucket_rows,
+                       bucket_signs, ws, ws_bytes, 0, stream);
+}
+
+int skh_hash_gen_variant(uint64_t seed, int64_t m, int32_t s, int64_t nrows, int64_t row0, int64_t blk,
+                         int64_t stride, int32_t* col_rows, int8_t* col_signs, int32_t* bucket_ptr,
+                         int32_t* bucket_rows, int8_t* bucket_signs, void* ws, size_t ws_bytes, void* stream) {
+  return hash_gen_impl(seed, m, s, nrows, row0, blk, stride, col_rows, col_signs, bucket_ptr, bucket_rows,
+                       bucket_signs, ws, ws_bytes, 1, stream);
 }
 
 int skh_hash_status(const void* ws, void* stream) {

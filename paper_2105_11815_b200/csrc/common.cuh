@@ -54,6 +54,9 @@ int launch_hash(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, in
                 int64_t stride, int32_t* col_rows, int8_t* col_signs, int32_t* bucket_ptr,
                 int32_t* bucket_rows, int8_t* bucket_signs, void* ws, size_t ws_bytes,
                 cudaStream_t st);
+int launch_hash_v(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, int64_t blk, int64_t stride,
+                  int32_t* col_rows, int8_t* col_signs, int32_t* bucket_ptr, int32_t* bucket_rows,
+                  int8_t* bucket_signs, void* ws, size_t ws_bytes, int variant, cudaStream_t st);
 int hash_status(const void* ws, cudaStream_t st);
 int64_t scan_scratch_ints(int64_t len);
 int launch_excl_scan_i32(int32_t* a, int64_t len, int32_t* blocksums, cudaStream_t st);

@@ -57,7 +57,7 @@ HashWs carve(void* ws, int64_t N) {
 template <int MAXS>
 __global__ void hash_kernel(uint64_t key, int64_t m, int s, int64_t nrows, int64_t row0, int64_t blk,
                             int64_t stride, int32_t* __restrict__ col_rows, int8_t* __restrict__ col_signs,
-                            uint64_t* __restrict__ keys, int32_t* __restrict__ status) {
+                            uint64_t* __restrict__ keys, int32_t* __restrict__ status, int variant) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nrows) return;
   const uint64_t j = (uint64_t)row_map(k, row0, blk, stride);
@@ -84,11 +84,11 @@ __global__ void hash_kernel(uint64_t key, int64_t m, int s, int64_t nrows, int64
     }
     const uint64_t u = stream_u(key, base + (uint64_t)t);
     const uint32_t r = (uint32_t)__umul64hi(u, (uint64_t)m);
-    bool dup = false;
+    bool dup = false;  // the s-hashing variant (Def. 7) keeps every draw
 #pragma unroll
     for (int q = 0; q < MAXS; ++q)
       if (q < na) dup |= (acc[q] == r);
-    if (!dup) {
+    if (variant || !dup) {
 #pragma unroll
       for (int q = 0; q < MAXS; ++q)
         if (q == na) acc[q] = r;
@@ -104,7 +104,23 @@ __global__ void hash_kernel(uint64_t key, int64_t m, int s, int64_t nrows, int64
       const int64_t e = k * s + q;
       if (col_rows) col_rows[e] = (int32_t)acc[q];
       if (col_signs) col_signs[e] = neg ? (int8_t)-1 : (int8_t)1;
-      keys[e] = ((uint64_t)acc[q] << 32) | ((uint64_t)((uint32_t)k << 1)) | neg;
+      // the radix sort is stable in the bucket digits only: a variant column's
+      // coincident draws must enter + before - (R18), so its keys are placed by
+      // their rank in (row, sign) order; for s-hashing the rows are distinct and
+      // the order is irrelevant
+      int pos = q;
+      if (variant) {
+        const uint64_t kq = ((uint64_t)acc[q] << 1) | neg;
+        pos = 0;
+#pragma unroll
+        for (int q2 = 0; q2 < MAXS; ++q2) {
+          if (q2 < s) {
+            const uint64_t k2 = ((uint64_t)acc[q2] << 1) | ((w >> q2) & 1ull);
+            pos += (k2 < kq) || (k2 == kq && q2 < q);
+          }
+        }
+      }
+      keys[k * s + pos] = ((uint64_t)acc[q] << 32) | ((uint64_t)((uint32_t)k << 1)) | neg;
     }
   }
 }
@@ -296,7 +312,7 @@ template <int MAXS>
 __global__ void hash_count_kernel(uint64_t key, int64_t m, int s, int64_t nrows, int64_t row0, int64_t blk,
                                   int64_t stride, int32_t* __restrict__ col_rows, int8_t* __restrict__ col_signs,
                                   int32_t* __restrict__ ebucket, uint32_t* __restrict__ ekey,
-                                  int32_t* __restrict__ counts, int32_t* __restrict__ status) {
+                                  int32_t* __restrict__ counts, int32_t* __restrict__ status, int variant) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nrows) return;
   const uint64_t j = (uint64_t)row_map(k, row0, blk, stride);
@@ -319,11 +335,11 @@ __global__ void hash_count_kernel(uint64_t key, int64_t m, int s, int64_t nrows,
         ++r;
       }
     }
-    bool dup = false;
+    bool dup = false;  // the s-hashing variant (Def. 7) keeps every draw
 #pragma unroll
     for (int q = 0; q < MAXS; ++q)
       if (q < na) dup |= (acc[q] == r);
-    if (!dup) {
+    if (variant || !dup) {
 #pragma unroll
       for (int q = 0; q < MAXS; ++q)
         if (q == na) acc[q] = r;
@@ -411,8 +427,8 @@ __global__ void __launch_bounds__(256) segsort_kernel(int64_t m, const int32_t* 
     // rank sort straight from global memory, keys are distinct
     for (int i = lane; i < L; i += 32) {
       const uint32_t x = tmp[beg + i];
-      int rank = 0;
-      for (int jx = 0; jx < L; ++jx) rank += tmp[beg + jx] < x;
+      int rank = 0;  // equal keys (a variant row drawn twice with one sign) by position
+      for (int jx = 0; jx < L; ++jx) rank += tmp[beg + jx] < x || (tmp[beg + jx] == x && jx < i);
       rows[beg + rank] = (int32_t)(x >> 1);
       signs[beg + rank] = (x & 1u) ? (int8_t)-1 : (int8_t)1;
     }
@@ -428,7 +444,7 @@ bool use_segmented(int64_t N, int64_t m) {
 
 int launch_hash_seg(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, int64_t blk, int64_t stride,
                     int32_t* col_rows, int8_t* col_signs, int32_t* bucket_ptr, int32_t* bucket_rows,
-                    int8_t* bucket_signs, const HashWs& w, int32_t* counts, cudaStream_t st) {
+                    int8_t* bucket_signs, const HashWs& w, int32_t* counts, int variant, cudaStream_t st) {
   const int64_t N = nrows * (int64_t)s;
   int32_t* ebucket = reinterpret_cast<int32_t*>(w.keys_a);
   uint32_t* ekey = reinterpret_cast<uint32_t*>(w.keys_a) + N;
@@ -439,7 +455,7 @@ int launch_hash_seg(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0
   const unsigned hb = (unsigned)((nrows + 255) / 256);
 #define SKH_HC(MS)                                                                                               \
   hash_count_kernel<MS><<<hb, 256, 0, st>>>(key, m, s, nrows, row0, blk, stride, col_rows, col_signs, ebucket, \
-                                            ekey, counts, w.status)
+                                            ekey, counts, w.status, variant)
   if (s <= 1) SKH_HC(1);
   else if (s <= 2) SKH_HC(2);
   else if (s <= 4) SKH_HC(4);
@@ -475,6 +491,16 @@ size_t hash_ws_bytes(int64_t nrows, int64_t m, int s) {
 int launch_hash(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, int64_t blk, int64_t stride,
                 int32_t* col_rows, int8_t* col_signs, int32_t* bucket_ptr, int32_t* bucket_rows,
                 int8_t* bucket_signs, void* ws, size_t ws_bytes, cudaStream_t st) {
+  return launch_hash_v(seed, m, s, nrows, row0, blk, stride, col_rows, col_signs, bucket_ptr, bucket_rows,
+                       bucket_signs, ws, ws_bytes, 0, st);
+}
+
+// variant != 0: the s-hashing variant (Def. def::s-hashing-variant, PAPER.md
+// L683-686): the s draws r_t, t = 0..s-1, are all kept (with replacement); a
+// row drawn twice appears twice in its bucket, + before - (R18).
+int launch_hash_v(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, int64_t blk, int64_t stride,
+                  int32_t* col_rows, int8_t* col_signs, int32_t* bucket_ptr, int32_t* bucket_rows,
+                  int8_t* bucket_signs, void* ws, size_t ws_bytes, int variant, cudaStream_t st) {
   const int64_t N = nrows * (int64_t)s;
   HashWs w = carve(ws, N);
   int32_t* counts = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + hash_ws_bytes(nrows, m, s) -
@@ -487,7 +513,7 @@ int launch_hash(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, in
   if (N > 0 && !force_radix && use_segmented(N, m)) {
     cudaMemsetAsync(w.status, 0, sizeof(int32_t), st);
     return launch_hash_seg(seed, m, s, nrows, row0, blk, stride, col_rows, col_signs, bucket_ptr, bucket_rows,
-                           bucket_signs, w, counts, st);
+                           bucket_signs, w, counts, variant, st);
   }
   cudaMemsetAsync(w.status, 0, sizeof(int32_t), st);
   if (N == 0) {
@@ -497,7 +523,8 @@ int launch_hash(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, in
   const uint64_t key = key_hash(seed);
   const unsigned hb = (unsigned)((nrows + 255) / 256);
 #define SKH_HASH_LAUNCH(MS) \
-  hash_kernel<MS><<<hb, 256, 0, st>>>(key, m, s, nrows, row0, blk, stride, col_rows, col_signs, w.keys_a, w.status)
+  hash_kernel<MS><<<hb, 256, 0, st>>>(key, m, s, nrows, row0, blk, stride, col_rows, col_signs, w.keys_a, w.status, \
+                                      variant)
   if (s <= 1) SKH_HASH_LAUNCH(1);
   else if (s <= 2) SKH_HASH_LAUNCH(2);
   else if (s <= 4) SKH_HASH_LAUNCH(4);

@@ -7,6 +7,9 @@ parity tests run the same launch configuration.
               into the first), R5 sketch_dense with alpha = c_ns (C2, C3HD, C5)
   PlainStep : R1+R2, R5 sketch_dense with alpha = c_s (C1, C3)
   CsrStep   : R1+R2, R5 sketch_csr (C4)
+  ColStep   : column-major A (the paper's LAPACK layout): one composite call
+              (skh_rht_dense_colmajor / skh_sketch_dense_colmajor); its stages
+              are timed by the library's stage trace (skh_trace_set)
 """
 import torch
 
@@ -147,3 +150,41 @@ class CsrStep:
         api.sketch_csr(self.bl, *self.csr, self.d, self.b, SA=self.SA, Sb=self.Sb, ws=self.ws)
         t.mark()
         return self.SA, self.Sb
+
+
+class ColStep:
+    """SA = S_h H D A (hd) or S A for a column-major A given as At (d, n)."""
+
+    def __init__(self, seed, At, b, m, s, hd, record=False):
+        self.seed, self.m, self.s, self.hd = seed, int(m), int(s), bool(hd)
+        self.At, self.b = At, b
+        d, n = At.shape
+        self.n, self.d = n, d
+        n_pad = 1
+        while n_pad < n:
+            n_pad *= 2
+        self.n_pad = n_pad
+        dev = At.device
+        self.SAt = torch.empty(d, self.m, dtype=torch.float64, device=dev)
+        self.Sb = torch.empty(self.m, dtype=torch.float64, device=dev) if b is not None else None
+        if self.hd:
+            self.op = api.RhtDenseColMajor(n, m, s, d, dev)
+        else:
+            lib = api._lib.load()
+            self.ws = api._workspace(lib.skh_sketch_dense_colmajor_workspace_bytes(n, m, s), dev)
+        self.record = record
+
+    def new_timer(self):
+        return api.Trace(16)
+
+    def run(self, timer=None):
+        if timer is None:
+            return self._call()
+        with timer:
+            return self._call()
+
+    def _call(self):
+        if self.hd:
+            return self.op(self.seed, self.At, self.b, SAt=self.SAt, Sb=self.Sb)
+        return api.sketch_dense_colmajor(self.seed, self.At, self.b, self.m, self.s, SAt=self.SAt, Sb=self.Sb,
+                                         ws=self.ws)
