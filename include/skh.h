@@ -295,6 +295,30 @@ int skh_rht_colmajor(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0,
                      const double* X, int64_t ldx, double* Y, int64_t ldy, int apply_diag,
                      void* stream);
 
+/* ======================================================================== *
+ * Algorithm 1 Steps 2-5 (L868-905): the least-squares solve preconditioned by
+ * the sketch.  Given Step 1's SA (m x d, row-major, ldsa >= d) and Sb for the
+ * row-major A (n x d, lda >= d) and b (n):
+ *   Step 2  SA = Q R, Householder QR (the full-rank DGEQRF mode the paper
+ *           allows, L1077; R19); SKH_EINVAL if some r_qq == 0;
+ *   Step 3  x_s = R^{-1} Q^T Sb; if ||A x_s - b|| <= tau_a: x = x_s, info[0] = 3;
+ *   Step 4  LSQR on W = A R^{-1} from y = 0 until the (7.1) estimate
+ *           ||W^T r|| / (||W|| ||r||) <= tau_r (L1085-1089) or it_max steps;
+ *   Step 5  x = R^{-1} y, info[0] = 4.
+ * Paper defaults (L1100-1102): tau_a = 1e-8, tau_r = 1e-6, it_max = 1e4.
+ * Outputs: x [d] (device), x_s [d] (device, nullable), info[2] (host:
+ * step, LSQR iterations), stats[3] (host: final (7.1) estimate, ||r|| estimate,
+ * ||A x_s - b||).  m >= d.  Each LSQR iteration streams A twice through the
+ * library's HBM kernels; the scalar recurrence runs on the host, so this call
+ * SYNCHRONISES `stream` (twice per iteration) and returns when x is ready.
+ * Deterministic: fixed-order reductions.  ws: skh_lls_workspace_bytes. */
+size_t skh_lls_workspace_bytes(int64_t n, int64_t d, int64_t m);
+int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const double* b,
+                  int64_t m, const double* SA, int64_t ldsa, const double* Sb,
+                  double tau_a, double tau_r, int64_t it_max,
+                  double* x, double* x_s, int64_t* info, double* stats,
+                  void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------------ *
  * Stage trace (thread-local).  After skh_trace_set(events, n) with n
  * caller-created cudaEvent_t handles (as void*), every composite entry point

@@ -392,3 +392,39 @@ class Trace:
         for i in range(1, self.count):
             out[self.names[i]] = out.get(self.names[i], 0.0) + self.events[i - 1].elapsed_time(self.events[i])
         return out
+
+
+# ---------------------------------------------------------------- Algorithm 1 Steps 2-5
+class LlsSolver:
+    """x ~ argmin ||A x - b|| from Step 1's SA, Sb (skh_lls_solve; row-major A).
+
+    Defaults are the paper's."""
+
+    def __init__(self, n, d, m, device=None):
+        lib = _lib.load()
+        self.n, self.d, self.m = int(n), int(d), int(m)
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        nb = lib.skh_lls_workspace_bytes(self.n, self.d, self.m)
+        if nb == 0:
+            raise ValueError("skh_lls_workspace_bytes failed: " + lib.skh_last_error().decode())
+        self.ws = _workspace(nb, device)
+
+    def __call__(self, A, b, SA, Sb, tau_a=1e-8, tau_r=1e-6, it_max=10000, x=None, x_s=None):
+        import ctypes
+        lib = _lib.load()
+        _need_cuda(A, b, SA, Sb)
+        if x is None:
+            x = torch.empty(self.d, dtype=torch.float64, device=A.device)
+        info = (ctypes.c_int64 * 2)()
+        stats = (ctypes.c_double * 3)()
+        rc = lib.skh_lls_solve(self.n, self.d, _ptr(A), _ld(A), _ptr(b), self.m, _ptr(SA), _ld(SA), _ptr(Sb),
+                               float(tau_a), float(tau_r), int(it_max), _ptr(x), _ptr(x_s), info, stats,
+                               _ptr(self.ws), self.ws.numel(), _stream())
+        _lib.check(rc, "skh_lls_solve")
+        return x, {"step": int(info[0]), "iters": int(info[1]), "test2": stats[0], "rnorm": stats[1],
+                   "res_s": stats[2]}
+
+
+def lls_solve(A, b, SA, Sb, **kw):
+    n, d = A.shape
+    return LlsSolver(n, d, SA.shape[0], A.device)(A, b, SA, Sb, **kw)

@@ -20,6 +20,9 @@ TARGETS = {
     os.path.join(PKG, "libskh.so"): sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu"))),
     os.path.join(ROOT, "synth", "libsynth.so"): sorted(glob.glob(os.path.join(ROOT, "synth", "csrc", "*.cu"))),
 }
+# extra link libraries: the LLS solve (csrc/lls.cu, Alg. 1 Steps 2-5) calls
+# cuSOLVER dgeqrf/dormqr and cuBLAS dtrsv for the small d x d factor work
+LIBS = {os.path.join(PKG, "libskh.so"): ["-lcusolver", "-lcublas"]}
 
 
 def _deps(srcs):
@@ -57,7 +60,7 @@ def build(force=False, verbose=False):
             if verbose:
                 sys.stderr.write(r.stderr)
             objs.append(o)
-        cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart", *LIBS.get(out, [])]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

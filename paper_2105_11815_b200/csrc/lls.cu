@@ -1,0 +1,536 @@
+// lls.cu -- Algorithm 1 Steps 2-5: the sketch-preconditioned
+// least-squares solve that consumes SA and Sb.
+//
+//  Step 2  SA = Q R (full-rank Householder QR, the Blendenpik/DGEQRF mode the
+//          paper allows, L1077; reading R19): cuSOLVER dgeqrf on a
+//          column-major copy of SA -- a small dense factorisation (m x d).
+//  Step 3  x_s = R^{-1} Q^T Sb (cuSOLVER dormqr + cuBLAS dtrsv, a back-solve,
+//          L1081); stop if ||A x_s - b|| <= tau_a.
+//  Step 4  LSQR (Paige & Saunders) on W = A R^{-1} from y = 0, stopped by the
+//          (7.1) estimate ||W^T r|| / (||W|| ||r||) <= tau_r (L1085-1089) or
+//          it_max.  Every iteration streams A twice -- u <- A (R^{-1} v) - alpha u
+//          and v <- R^{-T} (A^T u) - beta v -- through the two HBM-bound kernels
+//          below; the d x d triangular solves are cuBLAS dtrsv, the scalar
+//          recurrence runs on the host (two 8-byte read-backs per iteration).
+//  Step 5  x = R^{-1} y.
+//
+// Kernels (ours, deterministic: every reduction has a fixed order):
+//  gemv_n_kernel   out[i] = A[i,:] . t + beta * yin[i] for row-major A, one warp
+//                  per row (512-byte coalesced row segments, t staged in shared
+//                  memory), plus per-CTA partial sums of out[i]^2;
+//  gemv_t_kernel   partial[g][c] = sum_{i in row block g} A[i,c] u[i]: a CTA owns
+//                  a row block x 512-column tile, each thread two columns, rows
+//                  streamed 8 at a time; colsum_kernel adds the partials in g
+//                  order;
+//  norm / vector kernels on n- and d-vectors.
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace skh {
+namespace {
+
+constexpr int kRowsPerCta = 8;   // gemv_n: one warp per row, 8 warps
+constexpr int kTCols = 512;      // gemv_t column tile (256 threads x 2 columns)
+constexpr int kTRows = 8;        // gemv_t rows in flight per thread
+constexpr int kMaxSmemX = 12288; // gemv_n stages t in shared memory up to this d
+
+// out[i] = dot(A[i,:], t) + beta * yin[i]; sq[blockIdx] = sum over the CTA's rows of out^2
+template <bool SMEM>
+__global__ void __launch_bounds__(256) gemv_n_kernel(int64_t n, int64_t d, const double* __restrict__ A, int64_t lda,
+                                                     const double* __restrict__ t, double beta,
+                                                     const double* yin, double* out, double* __restrict__ sq,
+                                                     int64_t rows_per_cta) {
+  extern __shared__ double ts[];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  if (SMEM) {
+    for (int64_t c = threadIdx.x; c < d; c += blockDim.x) ts[c] = t[c];
+    __syncthreads();
+  }
+  const double* tv = SMEM ? ts : t;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(n, r0 + rows_per_cta);
+  const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0) && (d % 2 == 0);
+  double wsq = 0.0;
+  for (int64_t i = r0 + wp; i < r1; i += kRowsPerCta) {
+    const double* a = A + i * lda;
+    double acc0 = 0.0, acc1 = 0.0;
+    if (vec) {
+      const double2* a2 = reinterpret_cast<const double2*>(a);
+      for (int64_t c2 = lane; c2 < d / 2; c2 += 32) {
+        const double2 v = __ldg(a2 + c2);
+        acc0 = fma(v.x, tv[2 * c2], acc0);
+        acc1 = fma(v.y, tv[2 * c2 + 1], acc1);
+      }
+    } else {
+      for (int64_t c = lane; c < d; c += 32) acc0 = fma(__ldg(a + c), tv[c], acc0);
+    }
+    double acc = acc0 + acc1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const double o = yin ? fma(beta, yin[i], acc) : acc;
+      out[i] = o;
+      wsq = fma(o, o, wsq);
+    }
+  }
+  __shared__ double part[kRowsPerCta];
+  if (lane == 0) part[wp] = wsq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kRowsPerCta; ++w) s += part[w];
+    sq[blockIdx.x] = s;
+  }
+}
+
+// partial[g * d + c] = sum_{i in block g} A[i, c] * u[i]   (grid: nblk x ntc)
+__global__ void __launch_bounds__(256) gemv_t_kernel(int64_t n, int64_t d, const double* __restrict__ A, int64_t lda,
+                                                     const double* __restrict__ u, double* __restrict__ partial,
+                                                     int64_t rows_per_blk, int64_t ntc) {
+  const int64_t g = blockIdx.x / ntc, tc = blockIdx.x % ntc;
+  const int64_t c = tc * kTCols + 2 * threadIdx.x;
+  const int64_t r0 = g * rows_per_blk, r1 = min(n, r0 + rows_per_blk);
+  const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
+  double acc0 = 0.0, acc1 = 0.0;
+  if (c < d) {
+    const bool two = c + 1 < d;
+    for (int64_t i0 = r0; i0 < r1; i0 += kTRows) {
+      double x0[kTRows], x1[kTRows], uu[kTRows];
+#pragma unroll
+      for (int k = 0; k < kTRows; ++k) {
+        const int64_t i = i0 + k;
+        x0[k] = 0.0;
+        x1[k] = 0.0;
+        uu[k] = 0.0;
+        if (i < r1) {
+          const double* a = A + i * lda + c;
+          uu[k] = __ldg(u + i);
+          if (vec && two) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(a));
+            x0[k] = v.x;
+            x1[k] = v.y;
+          } else {
+            x0[k] = __ldg(a);
+            if (two) x1[k] = __ldg(a + 1);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kTRows; ++k) {
+        acc0 = fma(x0[k], uu[k], acc0);
+        acc1 = fma(x1[k], uu[k], acc1);
+      }
+    }
+    partial[g * d + c] = acc0;
+    if (two) partial[g * d + c + 1] = acc1;
+  }
+}
+
+// out[c] = alpha * (sum_g partial[g][c]) + beta * yin[c]   (g ascending)
+__global__ void colsum_kernel(int64_t nblk, int64_t d, const double* __restrict__ partial, double alpha, double beta,
+                              const double* yin, double* out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d) return;
+  double s = 0.0;
+  for (int64_t g = 0; g < nblk; ++g) s += partial[g * d + c];
+  out[c] = yin ? fma(beta, yin[c], alpha * s) : alpha * s;
+}
+
+// sq[blockIdx] = sum of x[i]^2 over a 4096-element chunk, fixed tree order
+__global__ void sqsum_kernel(int64_t n, const double* __restrict__ x, double* __restrict__ sq) {
+  __shared__ double sh[256];
+  const int64_t base = (int64_t)blockIdx.x * 4096;
+  double s = 0.0;
+  for (int k = 0; k < 16; ++k) {
+    const int64_t i = base + threadIdx.x + 256 * k;
+    if (i < n) s = fma(x[i], x[i], s);
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sq[blockIdx.x] = sh[0];
+}
+
+// *out = sum of parts[0..np) (one thread, ascending) -- the final deterministic reduction
+__global__ void sum_parts_kernel(int64_t np, const double* __restrict__ parts, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int64_t i = 0; i < np; ++i) s += parts[i];
+    *out = s;
+  }
+}
+
+__global__ void scale_vec_kernel(int64_t n, double* x, double a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] *= a;
+}
+
+// y += p * w;  w = v + q * w
+__global__ void lsqr_update_kernel(int64_t d, double* y, double* w, const double* v, double p, double q) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < d) {
+    const double wi = w[i];
+    y[i] = fma(p, wi, y[i]);
+    w[i] = fma(q, wi, v[i]);
+  }
+}
+
+// out = a * x + b * y
+__global__ void axpby_kernel(int64_t n, double a, const double* x, double b, const double* y, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = y ? fma(b, y[i], a * x[i]) : a * x[i];
+}
+
+// row-major m x d (ld ldsa) -> column-major m x d (ld m)
+__global__ void to_colmajor_kernel(int64_t m, int64_t d, const double* __restrict__ S, int64_t ld,
+                                   double* __restrict__ F) {
+  __shared__ double tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int64_t r = r0 + k, c = c0 + threadIdx.x;
+    tile[k][threadIdx.x] = (r < m && c < d) ? S[r * ld + c] : 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int64_t c = c0 + k, r = r0 + threadIdx.x;
+    if (r < m && c < d) F[c * m + r] = tile[threadIdx.x][k];
+  }
+}
+
+inline unsigned nblocks(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+// ---------------------------------------------------------------- library handles (per thread, per device)
+struct Handles {
+  cusolverDnHandle_t sol = nullptr;
+  cublasHandle_t blas = nullptr;
+  int dev = -1;
+};
+thread_local Handles g_h;
+
+int handles(cudaStream_t st, Handles** out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (g_h.dev != dev) {
+    if (g_h.sol) cusolverDnDestroy(g_h.sol);
+    if (g_h.blas) cublasDestroy(g_h.blas);
+    g_h = Handles{};
+    if (cusolverDnCreate(&g_h.sol) != CUSOLVER_STATUS_SUCCESS || cublasCreate(&g_h.blas) != CUBLAS_STATUS_SUCCESS) {
+      set_error("lls: cannot create cuSOLVER/cuBLAS handles");
+      return SKH_ECUDA;
+    }
+    cublasSetPointerMode(g_h.blas, CUBLAS_POINTER_MODE_HOST);
+    g_h.dev = dev;
+  }
+  cusolverDnSetStream(g_h.sol, st);
+  cublasSetStream(g_h.blas, st);
+  *out = &g_h;
+  return SKH_OK;
+}
+
+struct LlsWs {
+  double* F;       // SA column-major, factored in place [m x d]
+  double* tau;     // Householder scalars [d]
+  double* qtb;     // Q^T Sb [m]
+  double* u;       // [n]
+  double* v;       // [d]
+  double* w;       // [d]
+  double* y;       // [d]
+  double* t;       // [d]
+  double* xs;      // [d]
+  double* part;    // gemv_t partials [nblk x d]
+  double* sq;      // norm partials [max(nrb, nsq)]
+  double* scal;    // [8] device scalars
+  int* devinfo;
+  double* lwork;   // cuSOLVER workspace
+  int lwork_n;
+  int64_t nblk, nrb;
+  size_t total;
+};
+
+int64_t gemv_t_blocks(int64_t n, int64_t d) {
+  const int64_t ntc = (d + kTCols - 1) / kTCols;
+  const int64_t want = std::max<int64_t>(1, (148 * 8) / ntc);
+  return std::min<int64_t>(want, std::max<int64_t>(1, (n + 255) / 256));
+}
+
+LlsWs lls_layout(void* base, int64_t n, int64_t d, int64_t m, int lwork_n) {
+  LlsWs w{};
+  char* p = static_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* q = p ? p + off : nullptr;
+    off += align_up(bytes);
+    return q;
+  };
+  w.nblk = gemv_t_blocks(n, d);
+  w.nrb = (n + 255) / 256;  // gemv_n CTAs (rows_per_cta = 256)
+  const int64_t nsq = std::max<int64_t>(w.nrb, (n + 4095) / 4096 + 1);
+  w.F = (double*)take(sizeof(double) * (size_t)m * d);
+  w.tau = (double*)take(sizeof(double) * (size_t)d);
+  w.qtb = (double*)take(sizeof(double) * (size_t)m);
+  w.u = (double*)take(sizeof(double) * (size_t)n);
+  w.v = (double*)take(sizeof(double) * (size_t)d);
+  w.w = (double*)take(sizeof(double) * (size_t)d);
+  w.y = (double*)take(sizeof(double) * (size_t)d);
+  w.t = (double*)take(sizeof(double) * (size_t)d);
+  w.xs = (double*)take(sizeof(double) * (size_t)d);
+  w.part = (double*)take(sizeof(double) * (size_t)w.nblk * d);
+  w.sq = (double*)take(sizeof(double) * (size_t)nsq);
+  w.scal = (double*)take(sizeof(double) * 8);
+  w.devinfo = (int*)take(sizeof(int) * 4);
+  w.lwork = (double*)take(sizeof(double) * (size_t)std::max(lwork_n, 1));
+  w.lwork_n = lwork_n;
+  w.total = off;
+  return w;
+}
+
+int query_lwork(int64_t m, int64_t d, int* lw) {
+  Handles* h = nullptr;
+  int rc = handles(nullptr, &h);
+  if (rc) return rc;
+  int a = 0, b = 0;
+  if (cusolverDnDgeqrf_bufferSize(h->sol, (int)m, (int)d, nullptr, (int)m, &a) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDormqr_bufferSize(h->sol, CUBLAS_SIDE_LEFT, CUBLAS_OP_T, (int)m, 1, (int)d, nullptr, (int)m, nullptr,
+                                  nullptr, (int)m, &b) != CUSOLVER_STATUS_SUCCESS) {
+    set_error("lls: cuSOLVER workspace query failed");
+    return SKH_ECUDA;
+  }
+  *lw = std::max(a, b);
+  return SKH_OK;
+}
+
+// out = A t + beta yin (row-major A); returns ||out||^2 through w.scal[slot] (device)
+int gemv_n(int64_t n, int64_t d, const double* A, int64_t lda, const double* t, double beta, const double* yin,
+           double* out, const LlsWs& w, int slot, cudaStream_t st) {
+  const int64_t rows = 256;
+  const int64_t grid = (n + rows - 1) / rows;
+  if (d <= kMaxSmemX) {
+    const size_t smem = sizeof(double) * (size_t)d;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(gemv_n_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    gemv_n_kernel<true><<<(unsigned)grid, 256, smem, st>>>(n, d, A, lda, t, beta, yin, out, w.sq, rows);
+  } else {
+    gemv_n_kernel<false><<<(unsigned)grid, 256, 0, st>>>(n, d, A, lda, t, beta, yin, out, w.sq, rows);
+  }
+  note_launch();
+  sum_parts_kernel<<<1, 32, 0, st>>>(grid, w.sq, w.scal + slot);
+  note_launch();
+  return check_launch("gemv_n");
+}
+
+// out = alpha (A^T u) + beta yin
+int gemv_t(int64_t n, int64_t d, const double* A, int64_t lda, const double* u, double alpha, double beta,
+           const double* yin, double* out, const LlsWs& w, cudaStream_t st) {
+  const int64_t ntc = (d + kTCols - 1) / kTCols;
+  const int64_t rpb = (n + w.nblk - 1) / w.nblk;
+  gemv_t_kernel<<<(unsigned)(w.nblk * ntc), 256, 0, st>>>(n, d, A, lda, u, w.part, rpb, ntc);
+  note_launch();
+  colsum_kernel<<<nblocks(d), 256, 0, st>>>(w.nblk, d, w.part, alpha, beta, yin, out);
+  note_launch();
+  return check_launch("gemv_t");
+}
+
+int sqnorm(int64_t n, const double* x, const LlsWs& w, int slot, cudaStream_t st) {
+  const int64_t nb = (n + 4095) / 4096;
+  sqsum_kernel<<<(unsigned)nb, 256, 0, st>>>(n, x, w.sq);
+  note_launch();
+  sum_parts_kernel<<<1, 32, 0, st>>>(nb, w.sq, w.scal + slot);
+  note_launch();
+  return check_launch("sqnorm");
+}
+
+int read_scal(const LlsWs& w, int slot, double* out, cudaStream_t st) {
+  if (cudaMemcpyAsync(out, w.scal + slot, sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return check_launch("lls scalar read-back");
+  return SKH_OK;
+}
+
+int trsv(Handles* h, int64_t d, const LlsWs& w, int64_t m, bool trans, double* x) {
+  if (cublasDtrsv(h->blas, CUBLAS_FILL_MODE_UPPER, trans ? CUBLAS_OP_T : CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)d,
+                  w.F, (int)m, x, 1) != CUBLAS_STATUS_SUCCESS) {
+    set_error("lls: cublasDtrsv failed");
+    return SKH_ECUDA;
+  }
+  return SKH_OK;
+}
+
+}  // namespace
+}  // namespace skh
+
+using namespace skh;
+
+extern "C" {
+
+size_t skh_lls_workspace_bytes(int64_t n, int64_t d, int64_t m) {
+  if (n < 1 || d < 1 || m < d || m >= (1ll << 31)) return 0;
+  int lw = 0;
+  if (query_lwork(m, d, &lw)) return 0;
+  return lls_layout(nullptr, n, d, m, lw).total;
+}
+
+int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const double* b, int64_t m, const double* SA,
+                  int64_t ldsa, const double* Sb, double tau_a, double tau_r, int64_t it_max, double* x,
+                  double* x_s, int64_t* info, double* stats, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 1 || d < 1 || m < d || !A || !b || !SA || !Sb || !x || !info || !stats || it_max < 0 || tau_r < 0 ||
+      m >= (1ll << 31)) {
+    set_error("lls_solve: need n, d >= 1, m >= d, A, b, SA, Sb, x, info, stats, it_max >= 0");
+    return SKH_EINVAL;
+  }
+  if (lda < d || ldsa < d) {
+    set_error("lls_solve: lda/ldsa < d");
+    return SKH_EDIM;
+  }
+  int lw = 0;
+  int rc = query_lwork(m, d, &lw);
+  if (rc) return rc;
+  const LlsWs w = lls_layout(ws, n, d, m, lw);
+  if (!ws || ws_bytes < w.total) {
+    set_error("lls_solve workspace too small: need %zu bytes", w.total);
+    return SKH_EWORKSPACE;
+  }
+  cudaStream_t st = as_stream(stream);
+  Handles* h = nullptr;
+  rc = handles(st, &h);
+  if (rc) return rc;
+  skh_trace_start(st);
+  // ---- Step 2: SA = Q R
+  {
+    dim3 grid((unsigned)((d + 31) / 32), (unsigned)((m + 31) / 32));
+    to_colmajor_kernel<<<grid, dim3(32, 8), 0, st>>>(m, d, SA, ldsa, w.F);
+    note_launch();
+    if (cusolverDnDgeqrf(h->sol, (int)m, (int)d, w.F, (int)m, w.tau, w.lwork, w.lwork_n, w.devinfo) !=
+        CUSOLVER_STATUS_SUCCESS) {
+      set_error("lls: cusolverDnDgeqrf failed");
+      return SKH_ECUDA;
+    }
+  }
+  // rank check: the full-rank QR mode needs every r_qq != 0
+  {
+    std::vector<double> diag((size_t)d);
+    if (cudaMemcpy2DAsync(diag.data(), sizeof(double), w.F, sizeof(double) * (size_t)(m + 1), sizeof(double), d,
+                          cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return check_launch("lls: R diagonal");
+    for (int64_t q = 0; q < d; ++q) {
+      if (!(fabs(diag[q]) > 0.0)) {
+        set_error("lls: SA is rank deficient (r_%lld,%lld = %g); the full-rank QR mode needs rank d", (long long)q,
+                  (long long)q, diag[q]);
+        return SKH_EINVAL;
+      }
+    }
+  }
+  skh_trace_mark(st, "qr");
+  // ---- Step 3: x_s = R^{-1} Q^T Sb
+  cudaMemcpyAsync(w.qtb, Sb, sizeof(double) * (size_t)m, cudaMemcpyDeviceToDevice, st);
+  if (cusolverDnDormqr(h->sol, CUBLAS_SIDE_LEFT, CUBLAS_OP_T, (int)m, 1, (int)d, w.F, (int)m, w.tau, w.qtb, (int)m,
+                       w.lwork, w.lwork_n, w.devinfo) != CUSOLVER_STATUS_SUCCESS) {
+    set_error("lls: cusolverDnDormqr failed");
+    return SKH_ECUDA;
+  }
+  cudaMemcpyAsync(w.xs, w.qtb, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);
+  if ((rc = trsv(h, d, w, m, false, w.xs))) return rc;
+  if (x_s) cudaMemcpyAsync(x_s, w.xs, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);
+  if ((rc = gemv_n(n, d, A, lda, w.xs, -1.0, b, w.u, w, 0, st))) return rc;  // u = A x_s - b
+  double res2 = 0.0;
+  if ((rc = read_scal(w, 0, &res2, st))) return rc;
+  const double res_s = sqrt(res2);
+  stats[2] = res_s;
+  skh_trace_mark(st, "step3");
+  if (res_s <= tau_a) {
+    cudaMemcpyAsync(x, w.xs, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);
+    info[0] = 3;
+    info[1] = 0;
+    stats[0] = 0.0;
+    stats[1] = res_s;
+    return cudaStreamSynchronize(st) == cudaSuccess ? SKH_OK : check_launch("lls");
+  }
+  // ---- Step 4: LSQR on W = A R^{-1}, y0 = 0
+  double beta = 0.0, alpha = 0.0;
+  if ((rc = sqnorm(n, b, w, 1, st)) || (rc = read_scal(w, 1, &beta, st))) return rc;
+  beta = sqrt(beta);
+  cudaMemsetAsync(w.y, 0, sizeof(double) * (size_t)d, st);
+  int64_t it = 0;
+  double test2 = INFINITY, phibar = beta;
+  if (beta > 0.0) {
+    axpby_kernel<<<nblocks(n), 256, 0, st>>>(n, 1.0 / beta, b, 0.0, nullptr, w.u);  // u = b / beta
+    note_launch();
+    // v = R^{-T} A^T u
+    if ((rc = gemv_t(n, d, A, lda, w.u, 1.0, 0.0, nullptr, w.v, w, st))) return rc;
+    if ((rc = trsv(h, d, w, m, true, w.v))) return rc;
+    if ((rc = sqnorm(d, w.v, w, 1, st)) || (rc = read_scal(w, 1, &alpha, st))) return rc;
+    alpha = sqrt(alpha);
+  }
+  if (beta > 0.0 && alpha > 0.0) {
+    scale_vec_kernel<<<nblocks(d), 256, 0, st>>>(d, w.v, 1.0 / alpha);
+    note_launch();
+    cudaMemcpyAsync(w.w, w.v, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);
+    double rhobar = alpha, anorm2 = 0.0;
+    while (it < it_max) {
+      ++it;
+      // beta u = A (R^{-1} v) - alpha u
+      cudaMemcpyAsync(w.t, w.v, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);
+      if ((rc = trsv(h, d, w, m, false, w.t))) return rc;
+      if ((rc = gemv_n(n, d, A, lda, w.t, -alpha, w.u, w.u, w, 0, st))) return rc;
+      if ((rc = read_scal(w, 0, &beta, st))) return rc;
+      beta = sqrt(beta);
+      if (beta > 0.0) {
+        scale_vec_kernel<<<nblocks(n), 256, 0, st>>>(n, w.u, 1.0 / beta);
+        note_launch();
+      }
+      anorm2 = anorm2 + alpha * alpha + beta * beta;
+      // alpha v = R^{-T} (A^T u) - beta v
+      if ((rc = gemv_t(n, d, A, lda, w.u, 1.0, 0.0, nullptr, w.t, w, st))) return rc;
+      if ((rc = trsv(h, d, w, m, true, w.t))) return rc;
+      axpby_kernel<<<nblocks(d), 256, 0, st>>>(d, 1.0, w.t, -beta, w.v, w.v);
+      note_launch();
+      if ((rc = sqnorm(d, w.v, w, 1, st)) || (rc = read_scal(w, 1, &alpha, st))) return rc;
+      alpha = sqrt(alpha);
+      if (alpha > 0.0) {
+        scale_vec_kernel<<<nblocks(d), 256, 0, st>>>(d, w.v, 1.0 / alpha);
+        note_launch();
+      }
+      const double rho = sqrt(rhobar * rhobar + beta * beta);
+      const double c = rhobar / rho, s = beta / rho;
+      const double theta = s * alpha;
+      rhobar = -c * alpha;
+      const double phi = c * phibar;
+      phibar = s * phibar;
+      lsqr_update_kernel<<<nblocks(d), 256, 0, st>>>(d, w.y, w.w, w.v, phi / rho, -theta / rho);
+      note_launch();
+      const double arnorm = alpha * fabs(s * phi);
+      if (phibar == 0.0) {
+        test2 = 0.0;
+        break;
+      }
+      test2 = arnorm / (sqrt(anorm2) * phibar);
+      if (test2 <= tau_r) break;
+    }
+  } else {
+    test2 = 0.0;
+  }
+  skh_trace_mark(st, "lsqr");
+  // ---- Step 5: x = R^{-1} y
+  cudaMemcpyAsync(x, w.y, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);
+  if ((rc = trsv(h, d, w, m, false, x))) return rc;
+  info[0] = 4;
+  info[1] = it;
+  stats[0] = test2;
+  stats[1] = phibar;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("lls");
+  skh_trace_mark(st, "step5");
+  return SKH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,143 @@
+"""Algorithm 1 Steps 2-5 through the C ABI (skh_lls_solve) vs the
+oracle (oracle/lls.py) on the same SA, Sb (bit-identical to the oracle's by the
+sketch parity tests).  LSQR iterates are compared to rounding: the iteration
+count within 1 of the oracle's, the least-squares objective ||A x - b|| to 1e-10
+relative, Step 3's x_s (a direct solve) to 1e-10.  LSQR without
+reorthogonalisation amplifies the rounding differences of two implementations
+(cuSOLVER vs LAPACK QR, reduction orders): at exit both iterates are within the
+(7.1) tolerance of the solution but not of each other to rounding, so A x is
+compared to 10 tau_r relative (P:L1044-1050 bound the A-norm error by tau_r),
+and with tau_r -> 0 both must reach the least-squares solution (lstsq) to
+1e-9 kappa-scaled."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2105_11815_b200.build as b
+    b.build()
+
+
+def skh():
+    import paper_2105_11815_b200 as p
+    return p
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def ill_conditioned(n, d, seed, cond=1e4, noise=1.0):
+    r = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(r.standard_normal((n, d)))
+    V, _ = np.linalg.qr(r.standard_normal((d, d)))
+    A = (U * np.logspace(0, -np.log10(cond), d)) @ V.T
+    b = A @ r.standard_normal(d) + noise * r.standard_normal(n)
+    return A, b
+
+
+def compare(A, b, SA, Sb, cond=10.0, **kw):
+    from oracle import lls
+    At, bt = torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda()
+    xs = torch.empty(A.shape[1], dtype=torch.float64, device="cuda")
+    x, info = skh().LlsSolver(A.shape[0], A.shape[1], SA.shape[0])(At, bt, torch.from_numpy(SA).cuda(),
+                                                                   torch.from_numpy(Sb).cuda(), x_s=xs, **kw)
+    xo, io = lls.solve(A, b, SA, Sb, **kw)
+    assert info["step"] == io["step"]
+    assert rel(np_(xs), io["x_s"]) <= 1e-10
+    assert abs(info["res_s"] - io["res_s"]) <= 1e-10 * io["res_s"] + 1e-13 * np.linalg.norm(b)
+    assert abs(info["iters"] - io["iters"]) <= 1
+    tau_r = kw.get("tau_r", 1e-6)
+    if info["step"] == 4 and info["iters"] < kw.get("it_max", 10000):
+        assert rel(A @ np_(x), A @ xo) <= max(10 * tau_r, 1e-9)
+    if tau_r <= 1e-13:
+        xstar = np.linalg.lstsq(A, b, rcond=None)[0]
+        assert rel(np_(x), xstar) <= 1e-9 * max(1.0, cond / 1e3)
+    ro = np.linalg.norm(A @ xo - b)
+    assert abs(np.linalg.norm(A @ np_(x) - b) - ro) <= 1e-10 * max(ro, 1.0)
+    return info, io
+
+
+@pytest.mark.parametrize("n,d,m,s,cond", [(3000, 40, 120, 2, 1e3), (5000, 64, 109, 1, 1e6), (2000, 7, 14, 3, 10.0),
+                                          (4097, 33, 100, 2, 1e2)])
+def test_lls_vs_oracle_plain_hashing(n, d, m, s, cond):
+    from oracle import sketch
+    A, b = ill_conditioned(n, d, n + d, cond)
+    SA, Sb = sketch.sketch_dense(5, A, b, m, s)
+    info, io = compare(A, b, SA, Sb, cond=cond)
+    assert info["step"] == 4 and info["test2"] <= 1e-6
+
+
+def test_lls_hrht_paper_defaults():
+    """Ski-LLS-dense defaults: S_h H D with s = 1, m = 1.7 d."""
+    from oracle import sketch
+    r = np.random.default_rng(2)
+    n, d = 16384, 256
+    A = r.standard_normal((n, d))
+    b = r.standard_normal(n)
+    m = int(1.7 * d)
+    SA, Sb = skh().rht_dense(8, torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), m, 1)
+    SAo, Sbo = sketch.rht_sketch(8, A, b, m, 1)
+    assert np.array_equal(np_(SA), SAo) and np.array_equal(np_(Sb), Sbo)
+    compare(A, b, SAo, Sbo)
+
+
+def test_lls_step3_exit_consistent():
+    from oracle import sketch
+    A, b = ill_conditioned(3000, 20, 1, cond=10.0, noise=0.0)
+    SA, Sb = sketch.sketch_dense(3, A, b, 80, 2)
+    info, io = compare(A, b, SA, Sb, tau_a=1e-8)
+    assert info["step"] == 3 and info["iters"] == 0
+
+
+def test_lls_it_max_and_tau():
+    from oracle import sketch
+    A, b = ill_conditioned(2000, 30, 4, cond=1e5)
+    SA, Sb = sketch.sketch_dense(6, A, b, 90, 2)
+    for it_max in (0, 1, 3):
+        info, io = compare(A, b, SA, Sb, cond=1e5, it_max=it_max)
+        assert info["iters"] == io["iters"] == it_max
+    info, io = compare(A, b, SA, Sb, cond=1e5, tau_r=1e-14)
+    assert info["test2"] <= 1e-14
+
+
+def test_lls_rank_deficient_is_rejected():
+    from oracle import sketch
+    A, b = ill_conditioned(1000, 10, 5)
+    A[:, 3] = 0.0
+    SA, Sb = sketch.sketch_dense(1, A, b, 40, 2)
+    with pytest.raises(Exception, match="rank deficient"):
+        skh().lls_solve(torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), torch.from_numpy(SA).cuda(),
+                        torch.from_numpy(Sb).cuda())
+
+
+def test_lls_deterministic_and_C2_full_size():
+    """C2 at full size (65536 x 1024, m = 1792, S_h H D, s = 1) vs the oracle;
+    two runs bitwise equal."""
+    from oracle import lls
+    from synth import configs, device
+    cfg = configs.C2
+    A = device.dense(cfg)
+    b = device.rhs(cfg)
+    SA, Sb = skh().rht_dense(cfg.seed, A, b, cfg.m, cfg.s)
+    solver = skh().LlsSolver(cfg.n, cfg.d, cfg.m)
+    x1, i1 = solver(A, b, SA, Sb)
+    x1 = x1.clone()
+    x2, i2 = solver(A, b, SA, Sb)
+    assert torch.equal(x1, x2) and i1 == i2
+    xo, io = lls.solve(np_(A), np_(b), np_(SA), np_(Sb))
+    assert abs(i1["iters"] - io["iters"]) <= 1
+    An, bn = np_(A), np_(b)
+    ro = np.linalg.norm(An @ xo - bn)
+    assert abs(np.linalg.norm(An @ np_(x1) - bn) - ro) <= 1e-10 * ro
