@@ -296,6 +296,30 @@ int skh_rht_colmajor(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0,
                      void* stream);
 
 /* ======================================================================== *
+ * HR-DHT (eq. eqn::HR-DHT, "(6.1)", L1066-1075): SA = S_h F D A, Sb = S_h F D b
+ * with F the normalised Discrete Hartley Transform, F_ij = n^{-1/2}
+ * [cos + sin](2 pi (i-1)(j-1)/n) -- the sketch of the paper's Ski-LLS-dense.
+ * Any n (no padding): S_h hashes the n rows.  The transform is cuFFT's D2Z
+ * (Fhat y = Re X - Im X), its work area taken from `ws`; SA = c * (ascending-
+ * row signed sums of Fhat D A rows), c = 1/sqrt(n s) (R20).  FFT
+ * rounding differs from the oracle's: compared to 1e-12 relative Frobenius.
+ *   skh_hrdht_dense:          A row-major [n x d] (lda >= d), SA [m x d] (ldsa >= d), s <= 64
+ *   skh_hrdht_dense_colmajor: A column-major (lda >= n), SA column-major (ldsa >= m),
+ *                             s <= 8, m <= 65536
+ * b nullable, Sb required iff b.  ws: the matching query (holds two transformed
+ * copies of [A b]; creating the cuFFT plan needs the device). */
+size_t skh_hrdht_dense_workspace_bytes(int64_t n, int64_t m, int32_t s, int64_t d);
+int skh_hrdht_dense(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d,
+                    const double* A, int64_t lda, const double* b,
+                    double* SA, int64_t ldsa, double* Sb,
+                    void* ws, size_t ws_bytes, void* stream);
+size_t skh_hrdht_dense_colmajor_workspace_bytes(int64_t n, int64_t m, int32_t s, int64_t d);
+int skh_hrdht_dense_colmajor(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d,
+                             const double* A, int64_t lda, const double* b,
+                             double* SA, int64_t ldsa, double* Sb,
+                             void* ws, size_t ws_bytes, void* stream);
+
+/* ======================================================================== *
  * Algorithm 1 Steps 2-5 (L868-905): the least-squares solve preconditioned by
  * the sketch.  Given Step 1's SA (m x d, row-major, ldsa >= d) and Sb for the
  * row-major A (n x d, lda >= d) and b (n):

@@ -428,3 +428,44 @@ class LlsSolver:
 def lls_solve(A, b, SA, Sb, **kw):
     n, d = A.shape
     return LlsSolver(n, d, SA.shape[0], A.device)(A, b, SA, Sb, **kw)
+
+
+# ---------------------------------------------------------------- HR-DHT (eq. (6.1))
+def hrdht_dense(seed, A, b, m, s, SA=None, Sb=None, ws=None):
+    """SA = S_h F D A, Sb = S_h F D b with F the normalised DHT (any n); row-major A."""
+    lib = _lib.load()
+    _need_cuda(A, b)
+    n, d = A.shape
+    if SA is None:
+        SA = torch.empty(m, d, dtype=torch.float64, device=A.device)
+    if b is not None and Sb is None:
+        Sb = torch.empty(m, dtype=torch.float64, device=A.device)
+    if ws is None:
+        nb = lib.skh_hrdht_dense_workspace_bytes(n, int(m), int(s), d)
+        if nb == 0:
+            raise ValueError("skh_hrdht_dense_workspace_bytes failed: " + lib.skh_last_error().decode())
+        ws = _workspace(nb, A.device)
+    rc = lib.skh_hrdht_dense(int(seed) & (2**64 - 1), n, int(m), int(s), d, _ptr(A), _ld(A), _ptr(b), _ptr(SA),
+                             _ld(SA), _ptr(Sb), _ptr(ws), ws.numel(), _stream())
+    _lib.check(rc, "skh_hrdht_dense")
+    return SA, Sb
+
+
+def hrdht_dense_colmajor(seed, At, b, m, s, SAt=None, Sb=None, ws=None):
+    """Same for column-major A given as At (d, n); returns SA^T (d, m), Sb."""
+    lib = _lib.load()
+    _need_cuda(At, b)
+    d, n = At.shape
+    if SAt is None:
+        SAt = torch.empty(d, m, dtype=torch.float64, device=At.device)
+    if b is not None and Sb is None:
+        Sb = torch.empty(m, dtype=torch.float64, device=At.device)
+    if ws is None:
+        nb = lib.skh_hrdht_dense_colmajor_workspace_bytes(n, int(m), int(s), d)
+        if nb == 0:
+            raise ValueError("skh_hrdht_dense_colmajor_workspace_bytes failed: " + lib.skh_last_error().decode())
+        ws = _workspace(nb, At.device)
+    rc = lib.skh_hrdht_dense_colmajor(int(seed) & (2**64 - 1), n, int(m), int(s), d, _ptr(At), _ld_cm(At, n),
+                                      _ptr(b), _ptr(SAt), _ld_cm(SAt, m), _ptr(Sb), _ptr(ws), ws.numel(), _stream())
+    _lib.check(rc, "skh_hrdht_dense_colmajor")
+    return SAt, Sb

@@ -21,8 +21,9 @@ TARGETS = {
     os.path.join(ROOT, "synth", "libsynth.so"): sorted(glob.glob(os.path.join(ROOT, "synth", "csrc", "*.cu"))),
 }
 # extra link libraries: the LLS solve (csrc/lls.cu, Alg. 1 Steps 2-5) calls
-# cuSOLVER dgeqrf/dormqr and cuBLAS dtrsv for the small d x d factor work
-LIBS = {os.path.join(PKG, "libskh.so"): ["-lcusolver", "-lcublas"]}
+# cuSOLVER dgeqrf/dormqr and cuBLAS dtrsv for the small d x d factor work; the
+# HR-DHT sketch (csrc/dht.cu) calls cuFFT for the Hartley transform
+LIBS = {os.path.join(PKG, "libskh.so"): ["-lcusolver", "-lcublas", "-lcufft"]}
 
 
 def _deps(srcs):
