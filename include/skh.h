@@ -319,6 +319,19 @@ int skh_hrdht_dense_colmajor(uint64_t seed, int64_t n, int64_t m, int32_t s, int
                              double* SA, int64_t ldsa, double* Sb,
                              void* ws, size_t ws_bytes, void* stream);
 
+/* SR-DHT (eq. eq::SR-DHT, "(7.2)", L1285-1289; Blendenpik's sketch, the
+ * paper's comparison in Fig. 1): SA = S_s F D A, Sb = S_s F D b, where row r of
+ * the sampling matrix S_s selects column j_r = floor(u(mix64(seed ^
+ * 0x53414D50), r) * n / 2^64) with value 1 (independent draws, with
+ * replacement; R21).  Same transform as skh_hrdht_dense; SA[r, :] =
+ * n^{-1/2} (Fhat D A)[j_r, :].  Row-major A and SA.  No m limit but m >= 1;
+ * m < d is allowed (an underdetermined sketch). */
+size_t skh_srdht_dense_workspace_bytes(int64_t n, int64_t m, int64_t d);
+int skh_srdht_dense(uint64_t seed, int64_t n, int64_t m, int64_t d,
+                    const double* A, int64_t lda, const double* b,
+                    double* SA, int64_t ldsa, double* Sb,
+                    void* ws, size_t ws_bytes, void* stream);
+
 /* ======================================================================== *
  * Algorithm 1 Steps 2-5 (L868-905): the least-squares solve preconditioned by
  * the sketch.  Given Step 1's SA (m x d, row-major, ldsa >= d) and Sb for the

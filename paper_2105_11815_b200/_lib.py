@@ -63,6 +63,8 @@ SIGNATURES = {
     "skh_hrdht_dense_colmajor_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32, c_i64]),
     "skh_hrdht_dense_colmajor": (ctypes.c_int, [c_u64, c_i64, c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_p, c_i64, c_p,
                                                 c_p, c_sz, c_p]),
+    "skh_srdht_dense_workspace_bytes": (c_sz, [c_i64, c_i64, c_i64]),
+    "skh_srdht_dense": (ctypes.c_int, [c_u64, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_p, c_i64, c_p, c_p, c_sz, c_p]),
     "skh_lls_workspace_bytes": (c_sz, [c_i64, c_i64, c_i64]),
     "skh_lls_solve": (ctypes.c_int, [c_i64, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_d, c_d, c_i64, c_p,
                                      c_p, ctypes.POINTER(c_i64), ctypes.POINTER(c_d), c_p, c_sz, c_p]),

@@ -469,3 +469,23 @@ def hrdht_dense_colmajor(seed, At, b, m, s, SAt=None, Sb=None, ws=None):
                                       _ptr(b), _ptr(SAt), _ld_cm(SAt, m), _ptr(Sb), _ptr(ws), ws.numel(), _stream())
     _lib.check(rc, "skh_hrdht_dense_colmajor")
     return SAt, Sb
+
+
+def srdht_dense(seed, A, b, m, SA=None, Sb=None, ws=None):
+    """SR-DHT (Blendenpik, eq. (7.2)): SA = S_s F D A with uniform row sampling."""
+    lib = _lib.load()
+    _need_cuda(A, b)
+    n, d = A.shape
+    if SA is None:
+        SA = torch.empty(m, d, dtype=torch.float64, device=A.device)
+    if b is not None and Sb is None:
+        Sb = torch.empty(m, dtype=torch.float64, device=A.device)
+    if ws is None:
+        nb = lib.skh_srdht_dense_workspace_bytes(n, int(m), d)
+        if nb == 0:
+            raise ValueError("skh_srdht_dense_workspace_bytes failed: " + lib.skh_last_error().decode())
+        ws = _workspace(nb, A.device)
+    rc = lib.skh_srdht_dense(int(seed) & (2**64 - 1), n, int(m), d, _ptr(A), _ld(A), _ptr(b), _ptr(SA), _ld(SA),
+                             _ptr(Sb), _ptr(ws), ws.numel(), _stream())
+    _lib.check(rc, "skh_srdht_dense")
+    return SA, Sb

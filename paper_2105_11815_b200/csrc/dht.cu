@@ -102,6 +102,17 @@ __global__ void hartley_rm_kernel(int64_t n, int64_t d, const cufftDoubleComplex
   }
 }
 
+// SR-DHT (eq. (7.2)): SA[r, :] = alpha * H[j_r, :], Sb[r] = alpha * hb[j_r],
+// j_r = floor(u(mix64(seed ^ "SAMP"), r) * n / 2^64) (R21)
+__global__ void sample_rows_kernel(int64_t m, int64_t n, int64_t d, uint64_t skey, const double* __restrict__ H,
+                                   const double* __restrict__ hb, double* __restrict__ SA, int64_t ldsa,
+                                   double* __restrict__ Sb, double alpha) {
+  const int64_t r = blockIdx.x;
+  const int64_t j = (int64_t)__umul64hi(stream_u(skey, (uint64_t)r), (uint64_t)n);
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) SA[r * ldsa + c] = alpha * H[j * d + c];
+  if (Sb && threadIdx.x == 0) Sb[r] = alpha * hb[j];
+}
+
 // ---------------------------------------------------------------- cuFFT plans (per thread, device, n, batch)
 struct Plan {
   cufftHandle h = 0;
@@ -203,7 +214,7 @@ size_t ws_bytes_for(int64_t n, int64_t m, int32_t s, int64_t d, bool rowmajor) {
 
 int hrdht_run(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const double* A, int64_t lda,
               const double* b, double* SA, int64_t ldsa, double* Sb, void* ws, size_t ws_bytes, bool rowmajor,
-              cudaStream_t st) {
+              cudaStream_t st, bool sample = false) {
   int rc = check_args(n, m, s, d, rowmajor);
   if (rc) return rc;
   if (!A || !SA) {
@@ -226,9 +237,11 @@ int hrdht_run(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const d
     return SKH_EWORKSPACE;
   }
   skh_trace_start(st);
-  rc = launch_hash(seed, m, s, n, 0, 0, 0, w.col_rows, w.col_signs, w.ptr, w.rows, w.signs, w.hws,
-                   hash_ws_bytes(n, m, s), st);
-  if (rc) return rc;
+  if (!sample) {
+    rc = launch_hash(seed, m, s, n, 0, 0, 0, w.col_rows, w.col_signs, w.ptr, w.rows, w.signs, w.hws,
+                     hash_ws_bytes(n, m, s), st);
+    if (rc) return rc;
+  }
   if (!rowmajor && (rc = launch_cm_lists(w.col_rows, w.col_signs, s, m, 0, 12, n, (n + 4095) / 4096, w.lists, st)))
     return rc;
   skh_trace_mark(st, "hash_gen");
@@ -261,8 +274,15 @@ int hrdht_run(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const d
     note_launch();
     if ((rc = check_launch("hrdht: hartley"))) return rc;
     skh_trace_mark(st, "hartley");
-    if ((rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.H, d, SA, ldsa, c, st))) return rc;
-    if (b && (rc = launch_gather_vec(m, w.ptr, w.rows, w.signs, w.hb, Sb, c, st))) return rc;
+    if (sample) {
+      sample_rows_kernel<<<(unsigned)m, 256, 0, st>>>(m, n, d, mix64(seed ^ 0x53414D50ull), w.H, w.hb, SA, ldsa,
+                                                      b ? Sb : nullptr, 1.0 / sqrt((double)n));
+      note_launch();
+      if ((rc = check_launch("srdht: sample"))) return rc;
+    } else {
+      if ((rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.H, d, SA, ldsa, c, st))) return rc;
+      if (b && (rc = launch_gather_vec(m, w.ptr, w.rows, w.signs, w.hb, Sb, c, st))) return rc;
+    }
   } else {
     hartley_cm_kernel<<<(unsigned)((n * ncol + 255) / 256), 256, 0, st>>>(n, ncol, w.Z, w.Y);
     note_launch();
@@ -300,6 +320,19 @@ int skh_hrdht_dense_colmajor(uint64_t seed, int64_t n, int64_t m, int32_t s, int
                              int64_t lda, const double* b, double* SA, int64_t ldsa, double* Sb, void* ws,
                              size_t ws_bytes, void* stream) {
   return hrdht_run(seed, n, m, s, d, A, lda, b, SA, ldsa, Sb, ws, ws_bytes, false, as_stream(stream));
+}
+
+size_t skh_srdht_dense_workspace_bytes(int64_t n, int64_t m, int64_t d) {
+  return ws_bytes_for(n, m < 1 ? 1 : m, 1, d, true);
+}
+
+int skh_srdht_dense(uint64_t seed, int64_t n, int64_t m, int64_t d, const double* A, int64_t lda, const double* b,
+                    double* SA, int64_t ldsa, double* Sb, void* ws, size_t ws_bytes, void* stream) {
+  if (m >= (1ll << 31)) {
+    set_error("srdht: m too large");
+    return SKH_EOVERFLOW;
+  }
+  return hrdht_run(seed, n, m, 1, d, A, lda, b, SA, ldsa, Sb, ws, ws_bytes, true, as_stream(stream), true);
 }
 
 }  // extern "C"

@@ -85,3 +85,38 @@ def test_hrdht_C2_full_sampled_columns():
     assert rel(np_(SA[:, cols]), SAo) <= TOL
     _, Sbo = hartley.hrdht_sketch(cfg.seed, np.zeros((cfg.n, 1)), gen.rhs(cfg), cfg.m, cfg.s)
     assert rel(np_(Sb), Sbo) <= TOL
+
+
+@pytest.mark.parametrize("n,d,m", [(1, 1, 1), (100, 7, 30), (4000, 40, 700), (4097, 3, 5), (30000, 16, 50)])
+def test_srdht(n, d, m):
+    """SR-DHT (eq. (7.2)) vs oracle/sampling.py."""
+    from oracle import sampling
+    r = np.random.default_rng(n + d)
+    A = r.standard_normal((n, d))
+    b = r.standard_normal(n)
+    SA, Sb = skh().srdht_dense(21, torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), m)
+    SAo, Sbo = sampling.srdht_sketch(21, A, b, m)
+    assert rel(np_(SA), SAo) <= TOL and rel(np_(Sb), Sbo) <= TOL
+
+
+def test_fig1_claim_at_paper_size():
+    """Fig. 1 at the paper's size: coherent A = [I; 0] + 1e-8 J
+    (eq. (7.4)), n = 4000, d = 400.  With the GPU sketches, kappa(A R^{-1})
+    (QR without pivoting) is smaller with hashing (HR-DHT, s = 1) than with
+    sampling (SR-DHT) at m/d in {1.5, 2, 3} for the median over seeds, and the
+    hashing kappa at m/d = 1.5 is already modest."""
+    from oracle import sampling
+    n, d = 4000, 400
+    A = torch.from_numpy(sampling.coherent_A(n, d)).cuda()
+
+    def kappa(SA):
+        R = torch.linalg.qr(SA, mode="r")[1]
+        sv = torch.linalg.svdvals(torch.linalg.solve_triangular(R, A, upper=True, left=False))
+        return float(sv[0] / sv[-1])
+
+    for ratio in (1.5, 2.0, 3.0):
+        m = int(ratio * d)
+        kh = [kappa(skh().hrdht_dense(sd, A, None, m, 1)[0]) for sd in range(5)]
+        ks = [kappa(skh().srdht_dense(sd, A, None, m)[0]) for sd in range(5)]
+        assert np.median(kh) < np.median(ks)
+    assert np.median([kappa(skh().hrdht_dense(sd, A, None, 600, 1)[0]) for sd in range(5)]) < 20
