@@ -34,6 +34,14 @@ What each module computes (all fp64, plain NumPy, slow on purpose):
                   linearity, subspace-embedding band (R11),
                   negative control for coherent A without H D,
                   sketch-QR-preconditioned LSQR vs normal equations.
+* ``variant``   - the s-hashing variant T of Def. 7.  Pinned:
+                  Lemma 8, collision probability, s = 1 reduction.
+* ``lls``       - Algorithm 1 Steps 2-5: QR, x_s, LSQR with the
+                  (7.1) stop.  Pinned: scipy's LSQR, lstsq.
+* ``hartley``   - HR-DHT S_h F D (eq. (6.1)).  Pinned: explicit
+                  (6.1) matrix, involution, Parseval, n = 2 WHT identity.
+* ``sampling``  - SR-DHT S_s F D (eq. (7.2)) and the Fig. 1 experiment
+                  (P:L1284-1297).  Pinned: chi^2, collision rate, explicit S_s.
 * ``probes``    - Freivalds identities w^T(SA)v = (S^T w)^T(Av) for sizes the
                   oracle cannot materialise.  Pinned: equals the dense product on
                   small sizes.
