@@ -355,6 +355,15 @@ int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const doub
                   double tau_a, double tau_r, int64_t it_max,
                   double* x, double* x_s, int64_t* info, double* stats,
                   void* ws, size_t ws_bytes, void* stream);
+/* Same for column-major A (A[c*lda + i], lda >= n) and column-major SA
+ * (ldsa >= m) -- the output layout of skh_rht_dense_colmajor; same workspace
+ * query.  A x is one thread per row over the columns in order, A^T u partial
+ * dot products over 4096-row blocks summed in block order. */
+int skh_lls_solve_colmajor(int64_t n, int64_t d, const double* A, int64_t lda, const double* b,
+                           int64_t m, const double* SA, int64_t ldsa, const double* Sb,
+                           double tau_a, double tau_r, int64_t it_max,
+                           double* x, double* x_s, int64_t* info, double* stats,
+                           void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ *
  * Stage trace (thread-local).  After skh_trace_set(events, n) with n

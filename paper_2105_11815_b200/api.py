@@ -409,7 +409,8 @@ class LlsSolver:
             raise ValueError("skh_lls_workspace_bytes failed: " + lib.skh_last_error().decode())
         self.ws = _workspace(nb, device)
 
-    def __call__(self, A, b, SA, Sb, tau_a=1e-8, tau_r=1e-6, it_max=10000, x=None, x_s=None):
+    def __call__(self, A, b, SA, Sb, tau_a=1e-8, tau_r=1e-6, it_max=10000, x=None, x_s=None, colmajor=False):
+        """colmajor=True: A given as At (d, n) and SA as SAt (d, m) (skh_lls_solve_colmajor)."""
         import ctypes
         lib = _lib.load()
         _need_cuda(A, b, SA, Sb)
@@ -417,10 +418,16 @@ class LlsSolver:
             x = torch.empty(self.d, dtype=torch.float64, device=A.device)
         info = (ctypes.c_int64 * 2)()
         stats = (ctypes.c_double * 3)()
-        rc = lib.skh_lls_solve(self.n, self.d, _ptr(A), _ld(A), _ptr(b), self.m, _ptr(SA), _ld(SA), _ptr(Sb),
-                               float(tau_a), float(tau_r), int(it_max), _ptr(x), _ptr(x_s), info, stats,
-                               _ptr(self.ws), self.ws.numel(), _stream())
-        _lib.check(rc, "skh_lls_solve")
+        if colmajor:
+            rc = lib.skh_lls_solve_colmajor(self.n, self.d, _ptr(A), _ld_cm(A, self.n), _ptr(b), self.m, _ptr(SA),
+                                            _ld_cm(SA, self.m), _ptr(Sb), float(tau_a), float(tau_r), int(it_max),
+                                            _ptr(x), _ptr(x_s), info, stats, _ptr(self.ws), self.ws.numel(),
+                                            _stream())
+        else:
+            rc = lib.skh_lls_solve(self.n, self.d, _ptr(A), _ld(A), _ptr(b), self.m, _ptr(SA), _ld(SA), _ptr(Sb),
+                                   float(tau_a), float(tau_r), int(it_max), _ptr(x), _ptr(x_s), info, stats,
+                                   _ptr(self.ws), self.ws.numel(), _stream())
+        _lib.check(rc, "skh_lls_solve_colmajor" if colmajor else "skh_lls_solve")
         return x, {"step": int(info[0]), "iters": int(info[1]), "test2": stats[0], "rnorm": stats[1],
                    "res_s": stats[2]}
 

@@ -22,6 +22,10 @@
 //                  a row block x 512-column tile, each thread two columns, rows
 //                  streamed 8 at a time; colsum_kernel adds the partials in g
 //                  order;
+//  cm_av_kernel / cm_atu_kernel  the same two products for column-major A
+//                  (skh_lls_solve_colmajor): one thread per row over the
+//                  columns in order; per-column dot products over 4096-row
+//                  blocks (u staged in shared memory) + colsum;
 //  norm / vector kernels on n- and d-vectors.
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
@@ -142,6 +146,78 @@ __global__ void colsum_kernel(int64_t nblk, int64_t d, const double* __restrict_
   double s = 0.0;
   for (int64_t g = 0; g < nblk; ++g) s += partial[g * d + c];
   out[c] = yin ? fma(beta, yin[c], alpha * s) : alpha * s;
+}
+
+// ---- column-major A (n x d, A[c * lda + i]): the same two products
+// out[i] = sum_c A[i, c] t[c] + beta yin[i]: one thread per row, columns in
+// order (8 loads in flight), a warp reads 256 contiguous bytes of a column;
+// sq[blockIdx] = sum over the CTA's rows of out^2 (fixed order)
+template <bool SMEM>
+__global__ void __launch_bounds__(256) cm_av_kernel(int64_t n, int64_t d, const double* __restrict__ A, int64_t lda,
+                                                    const double* __restrict__ t, double beta, const double* yin,
+                                                    double* out, double* __restrict__ sq) {
+  extern __shared__ double ts[];
+  if (SMEM) {
+    for (int64_t c = threadIdx.x; c < d; c += blockDim.x) ts[c] = t[c];
+    __syncthreads();
+  }
+  const double* tv = SMEM ? ts : t;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double acc = 0.0;
+  if (i < n) {
+    const double* a = A + i;
+    int64_t c = 0;
+    for (; c + 8 <= d; c += 8) {
+      double x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = __ldg(a + (c + k) * lda);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc = fma(x[k], tv[c + k], acc);
+    }
+    for (; c < d; ++c) acc = fma(__ldg(a + c * lda), tv[c], acc);
+    if (yin) acc = fma(beta, yin[i], acc);
+    out[i] = acc;
+  }
+  __shared__ double part[256];
+  part[threadIdx.x] = acc * acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) part[threadIdx.x] += part[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sq[blockIdx.x] = part[0];
+}
+
+// partial[g * d + c] = sum over rows i of block g (kCmRows rows) of A[i, c] u[i]:
+// the block's u staged in shared memory, one warp per column (lanes stride the
+// contiguous rows, warp-tree reduction)
+constexpr int kCmRows = 4096;
+__global__ void __launch_bounds__(256) cm_atu_kernel(int64_t n, int64_t d, const double* __restrict__ A, int64_t lda,
+                                                     const double* __restrict__ u, double* __restrict__ partial,
+                                                     int64_t ncg) {
+  __shared__ double us[kCmRows];
+  const int64_t g = blockIdx.x / ncg, cg = blockIdx.x % ncg;
+  const int64_t r0 = g * kCmRows;
+  const int nr = (int)min((int64_t)kCmRows, n - r0);
+  for (int i = threadIdx.x; i < nr; i += blockDim.x) us[i] = u[r0 + i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int64_t cpg = (d + ncg - 1) / ncg;  // columns of this group
+  const int64_t cbeg = cg * cpg, cend = min(d, cbeg + cpg);
+  for (int64_t c = cbeg + wp; c < cend; c += 8) {
+    const double* a = A + c * lda + r0;
+    double acc0 = 0.0, acc1 = 0.0;
+    int i = lane;
+    for (; i + 32 < nr; i += 64) {
+      acc0 = fma(__ldg(a + i), us[i], acc0);
+      acc1 = fma(__ldg(a + i + 32), us[i + 32], acc1);
+    }
+    for (; i < nr; i += 32) acc0 = fma(__ldg(a + i), us[i], acc0);
+    double acc = acc0 + acc1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) partial[g * d + c] = acc;
+  }
 }
 
 // sq[blockIdx] = sum of x[i]^2 over a 4096-element chunk, fixed tree order
@@ -274,8 +350,9 @@ LlsWs lls_layout(void* base, int64_t n, int64_t d, int64_t m, int lwork_n) {
     return q;
   };
   w.nblk = gemv_t_blocks(n, d);
+  const int64_t nblk_cm = (n + kCmRows - 1) / kCmRows;  // column-major A^T u row blocks
   w.nrb = (n + 255) / 256;  // gemv_n CTAs (rows_per_cta = 256)
-  const int64_t nsq = std::max<int64_t>(w.nrb, (n + 4095) / 4096 + 1);
+  const int64_t nsq = std::max<int64_t>(w.nrb, (n + 4095) / 4096 + 1) + 1;
   w.F = (double*)take(sizeof(double) * (size_t)m * d);
   w.tau = (double*)take(sizeof(double) * (size_t)d);
   w.qtb = (double*)take(sizeof(double) * (size_t)m);
@@ -285,7 +362,7 @@ LlsWs lls_layout(void* base, int64_t n, int64_t d, int64_t m, int lwork_n) {
   w.y = (double*)take(sizeof(double) * (size_t)d);
   w.t = (double*)take(sizeof(double) * (size_t)d);
   w.xs = (double*)take(sizeof(double) * (size_t)d);
-  w.part = (double*)take(sizeof(double) * (size_t)w.nblk * d);
+  w.part = (double*)take(sizeof(double) * (size_t)std::max(w.nblk, nblk_cm) * d);
   w.sq = (double*)take(sizeof(double) * (size_t)nsq);
   w.scal = (double*)take(sizeof(double) * 8);
   w.devinfo = (int*)take(sizeof(int) * 4);
@@ -341,6 +418,40 @@ int gemv_t(int64_t n, int64_t d, const double* A, int64_t lda, const double* u, 
   return check_launch("gemv_t");
 }
 
+int sqnorm(int64_t n, const double* x, const LlsWs& w, int slot, cudaStream_t st);
+
+// out = A t + beta yin and ||out||^2 -> scal[slot], for either layout
+int apply_A(bool cm, int64_t n, int64_t d, const double* A, int64_t lda, const double* t, double beta,
+            const double* yin, double* out, const LlsWs& w, int slot, cudaStream_t st) {
+  if (!cm) return gemv_n(n, d, A, lda, t, beta, yin, out, w, slot, st);
+  const int64_t grid = (n + 255) / 256;
+  if (d <= kMaxSmemX) {
+    const size_t smem = sizeof(double) * (size_t)d;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(cm_av_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cm_av_kernel<true><<<(unsigned)grid, 256, smem, st>>>(n, d, A, lda, t, beta, yin, out, w.sq);
+  } else {
+    cm_av_kernel<false><<<(unsigned)grid, 256, 0, st>>>(n, d, A, lda, t, beta, yin, out, w.sq);
+  }
+  note_launch();
+  sum_parts_kernel<<<1, 32, 0, st>>>(grid, w.sq, w.scal + slot);
+  note_launch();
+  return check_launch("cm_av");
+}
+
+// out = A^T u + beta yin, for either layout
+int apply_AT(bool cm, int64_t n, int64_t d, const double* A, int64_t lda, const double* u, double beta,
+             const double* yin, double* out, const LlsWs& w, cudaStream_t st) {
+  if (!cm) return gemv_t(n, d, A, lda, u, 1.0, beta, yin, out, w, st);
+  const int64_t nblk = (n + kCmRows - 1) / kCmRows;
+  const int64_t ncg = std::max<int64_t>(1, std::min<int64_t>((d + 7) / 8, (148 * 8 + nblk - 1) / nblk));
+  cm_atu_kernel<<<(unsigned)(nblk * ncg), 256, 0, st>>>(n, d, A, lda, u, w.part, ncg);
+  note_launch();
+  colsum_kernel<<<nblocks(d), 256, 0, st>>>(nblk, d, w.part, 1.0, beta, yin, out);
+  note_launch();
+  return check_launch("cm_atu");
+}
+
 int sqnorm(int64_t n, const double* x, const LlsWs& w, int slot, cudaStream_t st) {
   const int64_t nb = (n + 4095) / 4096;
   sqsum_kernel<<<(unsigned)nb, 256, 0, st>>>(n, x, w.sq);
@@ -380,16 +491,17 @@ size_t skh_lls_workspace_bytes(int64_t n, int64_t d, int64_t m) {
   return lls_layout(nullptr, n, d, m, lw).total;
 }
 
-int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const double* b, int64_t m, const double* SA,
-                  int64_t ldsa, const double* Sb, double tau_a, double tau_r, int64_t it_max, double* x,
-                  double* x_s, int64_t* info, double* stats, void* ws, size_t ws_bytes, void* stream) {
+static int lls_solve_impl(bool cm, int64_t n, int64_t d, const double* A, int64_t lda, const double* b, int64_t m,
+                          const double* SA, int64_t ldsa, const double* Sb, double tau_a, double tau_r,
+                          int64_t it_max, double* x, double* x_s, int64_t* info, double* stats, void* ws,
+                          size_t ws_bytes, void* stream) {
   if (n < 1 || d < 1 || m < d || !A || !b || !SA || !Sb || !x || !info || !stats || it_max < 0 || tau_r < 0 ||
       m >= (1ll << 31)) {
     set_error("lls_solve: need n, d >= 1, m >= d, A, b, SA, Sb, x, info, stats, it_max >= 0");
     return SKH_EINVAL;
   }
-  if (lda < d || ldsa < d) {
-    set_error("lls_solve: lda/ldsa < d");
+  if ((!cm && (lda < d || ldsa < d)) || (cm && (lda < n || ldsa < m))) {
+    set_error(cm ? "lls_solve_colmajor: lda < n or ldsa < m" : "lls_solve: lda/ldsa < d");
     return SKH_EDIM;
   }
   int lw = 0;
@@ -407,9 +519,15 @@ int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const doub
   skh_trace_start(st);
   // ---- Step 2: SA = Q R
   {
-    dim3 grid((unsigned)((d + 31) / 32), (unsigned)((m + 31) / 32));
-    to_colmajor_kernel<<<grid, dim3(32, 8), 0, st>>>(m, d, SA, ldsa, w.F);
-    note_launch();
+    if (cm) {
+      if (cudaMemcpy2DAsync(w.F, sizeof(double) * (size_t)m, SA, sizeof(double) * (size_t)ldsa,
+                            sizeof(double) * (size_t)m, d, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return check_launch("lls: copy SA");
+    } else {
+      dim3 grid((unsigned)((d + 31) / 32), (unsigned)((m + 31) / 32));
+      to_colmajor_kernel<<<grid, dim3(32, 8), 0, st>>>(m, d, SA, ldsa, w.F);
+      note_launch();
+    }
     if (cusolverDnDgeqrf(h->sol, (int)m, (int)d, w.F, (int)m, w.tau, w.lwork, w.lwork_n, w.devinfo) !=
         CUSOLVER_STATUS_SUCCESS) {
       set_error("lls: cusolverDnDgeqrf failed");
@@ -442,7 +560,7 @@ int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const doub
   cudaMemcpyAsync(w.xs, w.qtb, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);
   if ((rc = trsv(h, d, w, m, false, w.xs))) return rc;
   if (x_s) cudaMemcpyAsync(x_s, w.xs, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);
-  if ((rc = gemv_n(n, d, A, lda, w.xs, -1.0, b, w.u, w, 0, st))) return rc;  // u = A x_s - b
+  if ((rc = apply_A(cm, n, d, A, lda, w.xs, -1.0, b, w.u, w, 0, st))) return rc;  // u = A x_s - b
   double res2 = 0.0;
   if ((rc = read_scal(w, 0, &res2, st))) return rc;
   const double res_s = sqrt(res2);
@@ -467,7 +585,7 @@ int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const doub
     axpby_kernel<<<nblocks(n), 256, 0, st>>>(n, 1.0 / beta, b, 0.0, nullptr, w.u);  // u = b / beta
     note_launch();
     // v = R^{-T} A^T u
-    if ((rc = gemv_t(n, d, A, lda, w.u, 1.0, 0.0, nullptr, w.v, w, st))) return rc;
+    if ((rc = apply_AT(cm, n, d, A, lda, w.u, 0.0, nullptr, w.v, w, st))) return rc;
     if ((rc = trsv(h, d, w, m, true, w.v))) return rc;
     if ((rc = sqnorm(d, w.v, w, 1, st)) || (rc = read_scal(w, 1, &alpha, st))) return rc;
     alpha = sqrt(alpha);
@@ -482,7 +600,7 @@ int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const doub
       // beta u = A (R^{-1} v) - alpha u
       cudaMemcpyAsync(w.t, w.v, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);
       if ((rc = trsv(h, d, w, m, false, w.t))) return rc;
-      if ((rc = gemv_n(n, d, A, lda, w.t, -alpha, w.u, w.u, w, 0, st))) return rc;
+      if ((rc = apply_A(cm, n, d, A, lda, w.t, -alpha, w.u, w.u, w, 0, st))) return rc;
       if ((rc = read_scal(w, 0, &beta, st))) return rc;
       beta = sqrt(beta);
       if (beta > 0.0) {
@@ -491,7 +609,7 @@ int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const doub
       }
       anorm2 = anorm2 + alpha * alpha + beta * beta;
       // alpha v = R^{-T} (A^T u) - beta v
-      if ((rc = gemv_t(n, d, A, lda, w.u, 1.0, 0.0, nullptr, w.t, w, st))) return rc;
+      if ((rc = apply_AT(cm, n, d, A, lda, w.u, 0.0, nullptr, w.t, w, st))) return rc;
       if ((rc = trsv(h, d, w, m, true, w.t))) return rc;
       axpby_kernel<<<nblocks(d), 256, 0, st>>>(d, 1.0, w.t, -beta, w.v, w.v);
       note_launch();
@@ -531,6 +649,21 @@ int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const doub
   if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("lls");
   skh_trace_mark(st, "step5");
   return SKH_OK;
+}
+
+int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const double* b, int64_t m, const double* SA,
+                  int64_t ldsa, const double* Sb, double tau_a, double tau_r, int64_t it_max, double* x,
+                  double* x_s, int64_t* info, double* stats, void* ws, size_t ws_bytes, void* stream) {
+  return lls_solve_impl(false, n, d, A, lda, b, m, SA, ldsa, Sb, tau_a, tau_r, it_max, x, x_s, info, stats, ws,
+                        ws_bytes, stream);
+}
+
+int skh_lls_solve_colmajor(int64_t n, int64_t d, const double* A, int64_t lda, const double* b, int64_t m,
+                           const double* SA, int64_t ldsa, const double* Sb, double tau_a, double tau_r,
+                           int64_t it_max, double* x, double* x_s, int64_t* info, double* stats, void* ws,
+                           size_t ws_bytes, void* stream) {
+  return lls_solve_impl(true, n, d, A, lda, b, m, SA, ldsa, Sb, tau_a, tau_r, it_max, x, x_s, info, stats, ws,
+                        ws_bytes, stream);
 }
 
 }  // extern "C"

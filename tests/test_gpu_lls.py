@@ -141,3 +141,41 @@ def test_lls_deterministic_and_C2_full_size():
     An, bn = np_(A), np_(b)
     ro = np.linalg.norm(An @ xo - bn)
     assert abs(np.linalg.norm(An @ np_(x1) - bn) - ro) <= 1e-10 * ro
+
+
+@pytest.mark.parametrize("n,d,m", [(3000, 40, 120), (8193, 17, 60), (20000, 130, 400)])
+def test_lls_colmajor_vs_oracle(n, d, m):
+    """skh_lls_solve_colmajor on a column-major A and SA (the layout of
+    skh_rht_dense_colmajor) against the oracle."""
+    from oracle import lls, sketch
+    A, b = ill_conditioned(n, d, n, 1e3)
+    SA, Sb = sketch.sketch_dense(2, A, b, m, 2)
+    At = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    SAt = torch.from_numpy(np.ascontiguousarray(SA.T)).cuda()
+    xs = torch.empty(d, dtype=torch.float64, device="cuda")
+    x, info = skh().LlsSolver(n, d, m)(At, torch.from_numpy(b).cuda(), SAt, torch.from_numpy(Sb).cuda(), x_s=xs,
+                                       colmajor=True)
+    xo, io = lls.solve(A, b, SA, Sb)
+    assert info["step"] == io["step"] == 4 and abs(info["iters"] - io["iters"]) <= 1
+    assert rel(np_(xs), io["x_s"]) <= 1e-10
+    assert rel(A @ np_(x), A @ xo) <= 1e-5
+    ro = np.linalg.norm(A @ xo - b)
+    assert abs(np.linalg.norm(A @ np_(x) - b) - ro) <= 1e-10 * ro
+
+
+def test_lls_colmajor_pipeline_hrht():
+    """The paper's layout end to end: skh_rht_dense_colmajor then the column-major
+    solve; the solution matches the row-major pipeline's objective."""
+    from synth import configs, device
+    cfg = configs.C2.scaled(n=1 << 15, d=128, m=224)
+    A = device.dense(cfg)
+    b = device.rhs(cfg)
+    At = A.t().contiguous()
+    SAt, Sb = skh().rht_dense_colmajor(cfg.seed, At, b, cfg.m, cfg.s)
+    x, info = skh().LlsSolver(cfg.n, cfg.d, cfg.m)(At, b, SAt, Sb, colmajor=True)
+    SA, Sb2 = skh().rht_dense(cfg.seed, A, b, cfg.m, cfg.s)
+    x2, info2 = skh().LlsSolver(cfg.n, cfg.d, cfg.m)(A, b, SA, Sb2)
+    r1 = torch.linalg.norm(A @ x - b).item()
+    r2 = torch.linalg.norm(A @ x2 - b).item()
+    assert info["step"] == 4 and abs(info["iters"] - info2["iters"]) <= 1
+    assert abs(r1 - r2) <= 1e-10 * r2
