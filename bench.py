@@ -297,9 +297,40 @@ def gpu_arm_single(args, cfg):
         line["e2e"] = e2e_measure(cfg, inputs, args.e2e_steps, torch, args.layout)
     del inputs
     torch.cuda.empty_cache()
+    if args.layout == "row" and cfg.kind != "csr" and cfg.hd and not args.no_alt_layout:
+        line["column_major"] = alt_layout_measure(args, cfg, torch, pk, src)
+        torch.cuda.empty_cache()
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
     print(json.dumps(line), flush=True)
+
+
+def alt_layout_measure(args, cfg, torch, pk, src):
+    """The same workload stored column-major (the paper's LAPACK layout): the
+    two-pass fused path of skh_rht_dense_colmajor, timed the
+    same way; reported beside the row-major headline."""
+    step, inputs = build_step(cfg, torch, "col")
+    torch.cuda.synchronize()
+    for _ in range(max(args.warmup, 0)):
+        step.run()
+    timers = [step.new_timer() for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(args.steps):
+        step.run(timers[k])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    per = [t.durations_ms() for t in timers]
+    stage_ms = {k: sum(p[k] for p in per) / len(per) for k in per[0]}
+    out = {"value": round(cfg.a_bytes / (ms / 1e3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
+           "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+           "roofline": roofline(cfg, step, stage_ms, pk["hbm_gbs"], src, "col"),
+           "note": "same A stored column-major; pass 1 (13 contiguous bits, D fused) + pass 2 fused with the "
+                   "gather: 3|A| of HBM traffic vs 7|A|; SA to 1e-12 (DESIGN.md R17)"}
+    del step, inputs
+    return out
 
 
 def main():
@@ -313,6 +344,8 @@ def main():
     ap.add_argument("--impl", default="skh", choices=["skh", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-alt-layout", action="store_true",
+                    help="skip the column-major measurement reported beside a row-major H D workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     from synth import configs
