@@ -63,6 +63,17 @@ def all_to_all(out, inp, group=None):
     return out
 
 
+def all_to_all_async(out, inp, group=None):
+    """Asynchronous all_to_all_single (NCCL: the collective runs on NCCL's stream
+    after the current stream's prior work; ``handle.wait()`` makes the current
+    stream wait for it).  gloo with CUDA tensors stages through host memory and
+    is synchronous (returns None)."""
+    if inp.is_cuda and dist.get_backend(group) == "gloo":
+        all_to_all(out, inp, group=group)
+        return None
+    return dist.all_to_all_single(out, inp, group=group, async_op=True)
+
+
 def _log2(x):
     k = int(x).bit_length() - 1
     if (1 << k) != x:
@@ -78,9 +89,18 @@ def strip_rows(m, G):
 
 class ShardedHrht:
     """SA = S_h H D A over G ranks holding contiguous row blocks of A (n = 2^k,
-    G = 2^g <= n).  run() returns this rank's strip (rows lo:hi of SA) and of Sb."""
+    G = 2^g <= n).  run() returns this rank's strip (rows lo:hi of SA) and of Sb.
 
-    def __init__(self, seed, A_loc, b_loc, n, m, s, ops=None, group=None):
+    Column-chunk pipeline (SURVEY §8(e) "Overlap: chunk the d axis"): H and S_h
+    act on every column independently, so the local transform, the butterfly
+    all-to-all (R7), the cross stages and the gather run per chunk of
+    ``chunk_cols`` columns, and the all-to-all of chunk k (asynchronous, NCCL's
+    stream) overlaps the cross stages + gather of chunk k - 1 and the local
+    transform of chunk k + 1 on the compute stream.  Two send and two receive
+    buffers of n/G x chunk_cols doubles (contiguous, so every destination's rows
+    are one contiguous block); the strip reduction (R6) follows the last chunk."""
+
+    def __init__(self, seed, A_loc, b_loc, n, m, s, ops=None, group=None, chunk_cols=None):
         self.ops = ops or CudaOps()
         self.group = group
         self.G = dist.get_world_size(group)
@@ -97,9 +117,12 @@ class ShardedHrht:
         self.A, self.b = A_loc, b_loc
         d = A_loc.shape[1]
         self.d = d
+        self.W = int(chunk_cols) if chunk_cols else (d if d <= 512 else 512)
+        self.K = (d + self.W - 1) // self.W
         kw = dict(dtype=A_loc.dtype, device=A_loc.device)
-        self.Y = torch.empty(self.L, d, **kw)
-        self.Y2 = torch.empty(self.L, d, **kw)
+        nb = min(2, self.K)
+        self.send = [torch.empty(self.L * self.W, **kw) for _ in range(nb)]
+        self.recv = [torch.empty(self.L * self.W, **kw) for _ in range(nb)]
         self.yb = torch.empty(self.L, 1, **kw) if b_loc is not None else None
         self.yb2 = torch.empty(self.L, 1, **kw) if b_loc is not None else None
         self.mq, self.strips = strip_rows(self.m, self.G)
@@ -113,9 +136,15 @@ class ShardedHrht:
         self.alpha = self.ops.c_ns(self.n, self.s)
         self.ws = None
         if isinstance(self.ops, CudaOps):
-            self.ws = self.ops.api.rht_stages_workspace(self.L, self.L, self.r * self.L, d, A_loc.device)
+            self.ws = self.ops.api.rht_stages_workspace(self.L, self.L, self.r * self.L, max(self.W, 1),
+                                                        A_loc.device)
 
-    STAGES = ("fwht_local", "all_to_all_rows", "fwht_cross", "hash_gen", "gather", "reduce")
+    STAGES = ("hash_gen", "rhs", "pipeline", "reduce")
+
+    def _chunk(self, k):
+        c0 = k * self.W
+        w = min(self.d, c0 + self.W) - c0
+        return c0, w
 
     def run(self, mark=None):
         """One sharded step; ``mark(name)`` (optional) is called after each of
@@ -123,35 +152,49 @@ class ShardedHrht:
         mark = mark or (lambda name: None)
         ops, G, r, L = self.ops, self.G, self.r, self.L
         blk = L // G
-        # R3 + R4 (local): global bits [0, log2 L) = local bits, D with global ids
-        ops.rht_stages(self.seed, self.A, 0, self.lg, L, r * L, True, self.Y, self.ws)
-        if self.b is not None:
-            ops.rht_stages(self.seed, self.b.view(-1, 1), 0, self.lg, L, r * L, True, self.yb, self.ws)
-        mark("fwht_local")
-        # R7: block q of rows [q*blk, (q+1)*blk) -> rank q (equal splits)
-        if G > 1:
-            all_to_all(self.Y2, self.Y, group=self.group)
-            if self.b is not None:
-                all_to_all(self.yb2, self.yb, group=self.group)
-        else:
-            self.Y2.copy_(self.Y)
-            if self.b is not None:
-                self.yb2.copy_(self.yb)
-        mark("all_to_all_rows")
-        # Y2 row k = g*blk + t holds global row g*L + r*blk + t; the rank bits g are
-        # local bits [log2 blk, log2 L): the remaining global stages, low to high.
-        if self.lq < self.lg:
-            ops.rht_stages(self.seed, self.Y2, self.lq, self.lg, L, 0, False, self.Y2, self.ws)
-            if self.b is not None:
-                ops.rht_stages(self.seed, self.yb2, self.lq, self.lg, L, 0, False, self.yb2, self.ws)
-        mark("fwht_cross")
-        # R1 + R2 for exactly these global rows (ascending in k)
+        # R1 + R2 for exactly the global rows this rank holds after the exchange:
+        # received row k = g*blk + t is global row g*L + r*blk + t (ascending in k)
         self.bl = ops.hash_gen(self.seed, self.m, self.s, L, r * blk, blk, L, out=self.bl)
         mark("hash_gen")
-        # R5: unscaled partial sums of this rank's rows
-        ops.sketch_dense(self.bl, self.Y2, None if self.b is None else self.yb2.view(-1), 1.0,
-                         SA=self.P[: self.m], Sb=None if self.b is None else self.Pb[: self.m])
-        mark("gather")
+        if self.b is not None:  # the right-hand side: one column, unpipelined
+            ops.rht_stages(self.seed, self.b.view(-1, 1), 0, self.lg, L, r * L, True, self.yb, self.ws)
+            if G > 1:
+                all_to_all(self.yb2, self.yb, group=self.group)
+            else:
+                self.yb2.copy_(self.yb)
+            if self.lq < self.lg:
+                ops.rht_stages(self.seed, self.yb2, self.lq, self.lg, L, 0, False, self.yb2, self.ws)
+            ops.sketch_dense(self.bl, self.yb2, None, 1.0, SA=self.Pb[: self.m].view(-1, 1))
+        mark("rhs")
+        handles = [None] * self.K
+
+        def finish(j):
+            c0, w = self._chunk(j)
+            if handles[j] is not None:
+                handles[j].wait()
+            Y2 = self.recv[j % len(self.recv)][: L * w].view(L, w)
+            # the rank bits g are local bits [log2 blk, log2 L): the remaining
+            # global stages, low to high
+            if self.lq < self.lg:
+                ops.rht_stages(self.seed, Y2, self.lq, self.lg, L, 0, False, Y2, self.ws)
+            # R5: unscaled partial sums of this rank's rows, columns c0 .. c0 + w
+            ops.sketch_dense(self.bl, Y2, None, 1.0, SA=self.P[: self.m, c0:c0 + w])
+
+        for k in range(self.K):
+            c0, w = self._chunk(k)
+            Y = self.send[k % len(self.send)][: L * w].view(L, w)
+            # R3 + R4 (local): global bits [0, log2 L) = local bits, D with global ids
+            ops.rht_stages(self.seed, self.A[:, c0:c0 + w], 0, self.lg, L, r * L, True, Y, self.ws)
+            # R7: block q of rows [q*blk, (q+1)*blk) -> rank q (equal splits)
+            Y2 = self.recv[k % len(self.recv)][: L * w].view(L, w)
+            if G > 1:
+                handles[k] = all_to_all_async(Y2, Y, group=self.group)
+            else:
+                Y2.copy_(Y)
+            if k >= 1:
+                finish(k - 1)
+        finish(self.K - 1)
+        mark("pipeline")
         # R6 (M5): strips to their owners, then a rank-order sum scaled once by c_ns
         lo, hi = self.strips[r]
         if G > 1:

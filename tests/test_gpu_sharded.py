@@ -37,7 +37,7 @@ def _worker(rank, G, port, kind, out_dir):
         L = n // G
         At = torch.from_numpy(A[rank * L:(rank + 1) * L].copy()).cuda()
         bt = torch.from_numpy(b[rank * L:(rank + 1) * L].copy()).cuda()
-        hr = sharded.ShardedHrht(seed, At, bt, n, m, s)
+        hr = sharded.ShardedHrht(seed, At, bt, n, m, s, chunk_cols=16)  # 4 column chunks through the pipeline
         strip, sb, lohi = hr.run()
         SA = sharded.gather_strips(strip, lohi, m).cpu().numpy()
         Sb = sharded.gather_strips(sb, lohi, m).cpu().numpy()

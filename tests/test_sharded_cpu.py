@@ -77,14 +77,15 @@ def _worker(rank, G, port, case):
     dist.init_process_group("gloo", rank=rank, world_size=G)
     try:
         from paper_2105_11815_b200 import sharded
-        n, d, m, s, seed, kind = case
+        n, d, m, s, seed, kind = case[:6]
+        chunk = case[6] if len(case) > 6 else None
         A = gen.small_int_dense(seed, n, d) if kind == "int" else np.random.default_rng(seed).standard_normal((n, d))
         b = np.random.default_rng(seed + 1).standard_normal(n) if kind != "int" else gen.small_int_dense(seed + 1, n, 1)[:, 0]
         ops = OracleOps()
         L = n // G
         At = torch.from_numpy(A[rank * L:(rank + 1) * L].copy())
         bt = torch.from_numpy(b[rank * L:(rank + 1) * L].copy())
-        hr = sharded.ShardedHrht(seed, At, bt, n, m, s, ops=ops)
+        hr = sharded.ShardedHrht(seed, At, bt, n, m, s, ops=ops, chunk_cols=chunk)
         strip, sb, (lo, hi) = hr.run()
         SA = sharded.gather_strips(strip, (lo, hi), m).numpy()
         Sb = sharded.gather_strips(sb, (lo, hi), m).numpy()
@@ -111,7 +112,9 @@ def _worker(rank, G, port, case):
 
 
 @pytest.mark.parametrize("G,case", [(2, (256, 8, 21, 1, 5, "real")), (2, (512, 6, 40, 2, 6, "int")),
-                                    (4, (1024, 5, 33, 1, 7, "real")), (4, (256, 4, 17, 3, 8, "int"))])
+                                    (4, (1024, 5, 33, 1, 7, "real")), (4, (256, 4, 17, 3, 8, "int")),
+                                    # column-chunk pipeline: 3 chunks (2 + 2 + 1 ragged), both buffers reused
+                                    (2, (512, 5, 30, 1, 9, "real", 2)), (4, (256, 7, 19, 2, 10, "int", 3))])
 def test_sharded_gloo(G, case):
     mp.spawn(_worker, args=(G, _free_port(), case), nprocs=G, join=True)
 
