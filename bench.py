@@ -222,9 +222,18 @@ def roofline(cfg, step, stage_ms, peak_gbs, peak_src, layout="row"):
         name = max((k for k in stage_ms if k in alg), key=lambda k: stage_ms[k])
         t = stage_ms[name]
         achieved = alg[name] / (t / 1e3) / 1e9
+        traffic, tsrc = None, None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                ent = json.load(f).get(cfg.name + "-col")
+            if ent and ent["kernel"] == "cm_" + name:
+                traffic, tsrc = ent["dram_bytes_per_launch"], ent["source"]
         return {"bound": "hbm", "kernel": "cm_" + name, "achieved": round(achieved, 1), "peak": peak_gbs,
-                "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": None, "traffic_source": None,
-                "alg_bytes_per_launch": alg[name], "ms_per_launch": round(t, 4), "peak_source": peak_src}
+                "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": traffic, "traffic_source": tsrc,
+                "alg_bytes_per_launch": alg[name], "ms_per_launch": round(t, 4), "peak_source": peak_src,
+                "note": "bound on chip: the rank-round scatter into shared memory (DESIGN.md §5b); DRAM traffic "
+                        "equals the algorithmic bytes"}
     if cfg.kind == "csr":
         name = "gather_csr"
         nnz = cfg.n * cfg.nnz_row
