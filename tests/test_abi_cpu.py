@@ -91,3 +91,44 @@ def test_product_has_no_fallback():
         p.api._need_cuda(torch.zeros(2))
     src = open(os.path.join(ROOT, "paper_2105_11815_b200", "api.py")).read()
     assert "oracle" not in src.replace("oracle side", "")
+
+
+def test_error_codes_widened_entry_points(lib):
+    """Validation of the column-major, variant, HR-DHT/SR-DHT and solve entry
+    points (argument checks run before any CUDA work)."""
+    EINVAL, ENOTPOW2, EDIM, EOVERFLOW, EWS = 1, 2, 3, 5, 6
+    p = ctypes.c_void_p(8)
+    # variant: the same argument rules as skh_hash_gen
+    assert lib.skh_hash_gen_variant(1, 4, 5, 10, 0, 0, 0, None, None, p, p, p, p, 1 << 20, None) == EINVAL
+    assert lib.skh_hash_gen_variant(1, 8, 2, 10, 0, 0, 0, None, None, p, p, p, None, 0, None) == EWS
+    # column-major HRHT: s <= 8, m <= 65536, lda >= n, ldsa >= m, Sb with b, workspace
+    assert lib.skh_rht_dense_colmajor(1, 100, 40, 9, 4, p, 100, None, p, 40, None, p, 1 << 30, None) == EINVAL
+    assert lib.skh_rht_dense_colmajor(1, 100, 70000, 1, 4, p, 100, None, p, 70000, None, p, 1 << 30, None) == EINVAL
+    assert lib.skh_rht_dense_colmajor(1, 100, 40, 1, 4, p, 99, None, p, 40, None, p, 1 << 30, None) == EDIM
+    assert lib.skh_rht_dense_colmajor(1, 100, 40, 1, 4, p, 100, None, p, 39, None, p, 1 << 30, None) == EDIM
+    assert lib.skh_rht_dense_colmajor(1, 100, 40, 1, 4, p, 100, p, p, 40, None, p, 1 << 30, None) == EDIM
+    assert lib.skh_rht_dense_colmajor(1, 100, 40, 1, 4, p, 100, None, p, 40, None, p, 64, None) == EWS
+    assert lib.skh_sketch_dense_colmajor(1, 100, 40, 2, 4, p, 50, None, p, 40, None, p, 1 << 30, None) == EDIM
+    assert lib.skh_sketch_dense_colmajor(1, 100, 40, 2, 4, p, 100, None, p, 40, None, p, 16, None) == EWS
+    # rht_colmajor: nrows must be a power of two, ld rules
+    assert lib.skh_rht_colmajor(1, 12, 12, 0, 2, p, 12, p, 12, 1, None) == ENOTPOW2
+    assert lib.skh_rht_colmajor(1, 16, 12, 0, 2, p, 11, p, 16, 1, None) == EDIM
+    assert lib.skh_rht_colmajor(1, 16, 17, 0, 2, p, 17, p, 16, 1, None) == EINVAL
+    # HR-DHT: s > 64 (row-major) / s > 8 (column-major), n*s overflow
+    assert lib.skh_hrdht_dense(1, 100, 70, 65, 4, p, 4, None, p, 4, None, p, 1 << 30, None) == EINVAL
+    assert lib.skh_hrdht_dense_colmajor(1, 100, 40, 9, 4, p, 100, None, p, 40, None, p, 1 << 30, None) == EINVAL
+    assert lib.skh_hrdht_dense(1, 1 << 30, 70, 3, 4, p, 4, None, p, 4, None, p, 1 << 30, None) == EOVERFLOW
+    assert lib.skh_srdht_dense(1, 100, 1 << 31, 4, p, 4, None, p, 4, None, p, 1 << 30, None) == EOVERFLOW
+    # solve: m < d, missing outputs, ld rules
+    info = (ctypes.c_int64 * 2)()
+    stats = (ctypes.c_double * 3)()
+    assert lib.skh_lls_solve(100, 10, p, 10, p, 9, p, 10, p, 1e-8, 1e-6, 10, p, None, info, stats, p, 1 << 30,
+                             None) == EINVAL
+    assert lib.skh_lls_solve(100, 10, p, 9, p, 20, p, 10, p, 1e-8, 1e-6, 10, p, None, info, stats, p, 1 << 30,
+                             None) == EDIM
+    assert lib.skh_lls_solve_colmajor(100, 10, p, 99, p, 20, p, 20, p, 1e-8, 1e-6, 10, p, None, info, stats, p,
+                                      1 << 30, None) == EDIM
+    assert lib.skh_lls_solve(100, 10, p, 10, p, 20, p, 10, p, 1e-8, -1.0, 10, p, None, info, stats, p, 1 << 30,
+                             None) == EINVAL
+    assert lib.skh_trace_set(None, -1) == EINVAL
+    assert lib.skh_trace_set(None, 0) == 0 and lib.skh_trace_count() == 0
