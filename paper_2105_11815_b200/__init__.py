@@ -6,4 +6,4 @@ multi-GPU sequencing (``sharded``).  See DESIGN.md.
 """
 from .api import (BucketLists, RhtDense, RhtDenseColMajor, SketchDenseHost, Trace, c_n, c_ns, c_s,  # noqa: F401
                   hash_gen, hash_status, hrdht_dense, hrdht_dense_colmajor, LlsSolver, lls_solve, ordered_sum, rht_colmajor, rht_dense, rht_dense_colmajor, rht_stages,
-                  scale, sketch_csr, sketch_dense, sketch_dense_colmajor, srdht_dense)
+                  scale, ski_lls_dense, sketch_csr, sketch_dense, sketch_dense_colmajor, srdht_dense)

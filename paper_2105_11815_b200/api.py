@@ -6,6 +6,7 @@ current stream.  Raises on a missing library or non-CUDA tensors.
 Citations (PAPER.md lines): Alg. 1 Step 1 L871; s-hashing L269-272; HRHT
 L790-801.
 """
+import math
 from dataclasses import dataclass
 
 import torch
@@ -496,3 +497,20 @@ def srdht_dense(seed, A, b, m, SA=None, Sb=None, ws=None):
                              _ptr(Sb), _ptr(ws), ws.numel(), _stream())
     _lib.check(rc, "skh_srdht_dense")
     return SA, Sb
+
+
+def ski_lls_dense(A, b, m=None, s=1, seed=0, transform="dht", tau_a=1e-8, tau_r=1e-6, it_max=10000):
+    """Ski-LLS-dense: Step 1 with the paper's dense sketch
+    S = S_h F D (transform="dht", eq. (6.1)) or the HRHT S_h H D (transform="wht",
+    Def. def::HRHT), then Steps 2-5 (skh_lls_solve).  Defaults are the paper's:
+    m = 1.7 d, s = 1, tau_a = 1e-8, tau_r = 1e-6, it_max = 1e4.
+    Row-major A.  Returns (x, info)."""
+    n, d = A.shape
+    m = int(m) if m is not None else max(d, int(math.ceil(1.7 * d)))
+    if transform == "dht":
+        SA, Sb = hrdht_dense(seed, A, b, m, s)
+    elif transform == "wht":
+        SA, Sb = rht_dense(seed, A, b, m, s)
+    else:
+        raise ValueError("transform must be 'dht' or 'wht'")
+    return LlsSolver(n, d, m, A.device)(A, b, SA, Sb, tau_a=tau_a, tau_r=tau_r, it_max=it_max)

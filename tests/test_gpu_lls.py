@@ -179,3 +179,20 @@ def test_lls_colmajor_pipeline_hrht():
     r2 = torch.linalg.norm(A @ x2 - b).item()
     assert info["step"] == 4 and abs(info["iters"] - info2["iters"]) <= 1
     assert abs(r1 - r2) <= 1e-10 * r2
+
+
+@pytest.mark.parametrize("transform", ["dht", "wht"])
+def test_ski_lls_dense_composite(transform):
+    """Ski-LLS-dense end to end with the paper's defaults (m = 1.7 d, s = 1):
+    the objective matches the least-squares optimum to 1e-10 relative
+    (tau_r = 1e-6 bounds the A-norm error)."""
+    r = np.random.default_rng(11)
+    n, d = 10000, 64
+    A = r.standard_normal((n, d)) @ np.diag(np.logspace(0, 3, d))
+    b = r.standard_normal(n)
+    x, info = skh().ski_lls_dense(torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), seed=3,
+                                  transform=transform)
+    xs = np.linalg.lstsq(A, b, rcond=None)[0]
+    best = np.linalg.norm(A @ xs - b)
+    assert info["step"] == 4 and info["test2"] <= 1e-6
+    assert np.linalg.norm(A @ np_(x) - b) <= best * (1 + 1e-10)
