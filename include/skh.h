@@ -159,7 +159,7 @@ int skh_sketch_dense(int64_t m, int32_t s,
  *   The bucket lists must be complete lists over all nrows rows (each row in
  *   exactly s buckets); bucket_ptr may be an offset view of m consecutive
  *   buckets of them (a bucket strip).  ws: skh_sketch_csr_workspace_bytes
- *   (the expanded (column, value) list of S.A, 12 * s * nnz bytes + 8 * nrows * s).
+ *   (the expanded (column, value) list of S.A, 12 * s * nnz bytes + 16 * nrows * s).
  *   Errors: SKH_EOVERFLOW if s * nnz >= 2^31.
  * ------------------------------------------------------------------------ */
 size_t skh_sketch_csr_workspace_bytes(int64_t nrows, int32_t s, int64_t nnz);

@@ -35,6 +35,7 @@ constexpr int kFree = 0x7fffffff;
 
 struct CsrWs {
   int32_t* off;   // [N + 1] exclusive scan of row lengths in bucket order
+  int64_t* rst;   // [N] row start (row_ptr[row]) of every bucket entry
   int32_t* bs;    // scan scratch
   int32_t* ecol;  // [s * nnz]
   double* eval;   // [s * nnz]
@@ -45,6 +46,8 @@ CsrWs csr_carve(void* ws, int64_t N, int64_t nexp) {
   char* p = static_cast<char*>(ws);
   w.off = reinterpret_cast<int32_t*>(p);
   p += align_up(sizeof(int32_t) * (size_t)(N + 1));
+  w.rst = reinterpret_cast<int64_t*>(p);
+  p += align_up(sizeof(int64_t) * (size_t)std::max<int64_t>(N, 1));
   w.bs = reinterpret_cast<int32_t*>(p);
   p += align_up(sizeof(int32_t) * (size_t)scan_scratch_ints(N + 1));
   w.eval = reinterpret_cast<double*>(p);
@@ -53,8 +56,10 @@ CsrWs csr_carve(void* ws, int64_t N, int64_t nexp) {
   return w;
 }
 
+// Row lengths in bucket order (scanned into off) and each entry's row start, so
+// the expand reads both coalesced instead of two random row_ptr words per entry.
 __global__ void csr_len_kernel(int64_t N, const int32_t* __restrict__ brow, const int64_t* __restrict__ row_ptr,
-                               int32_t* __restrict__ off) {
+                               int32_t* __restrict__ off, int64_t* __restrict__ rst) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t > N) return;
   if (t == N) {
@@ -62,24 +67,27 @@ __global__ void csr_len_kernel(int64_t N, const int32_t* __restrict__ brow, cons
     return;
   }
   const int r = brow[t];
-  off[t] = (int32_t)(row_ptr[r + 1] - row_ptr[r]);
+  const int64_t a = row_ptr[r];
+  off[t] = (int32_t)(row_ptr[r + 1] - a);
+  rst[t] = a;
 }
 
-__global__ void __launch_bounds__(256, 6) csr_expand_kernel(int64_t N, const int32_t* __restrict__ brow, const int8_t* __restrict__ bsg,
-                                  const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
-                                  const double* __restrict__ val, const int32_t* __restrict__ off,
-                                  int32_t* __restrict__ ecol, double* __restrict__ eval) {
+__global__ void __launch_bounds__(256, 6) csr_expand_kernel(int64_t N, const int8_t* __restrict__ bsg,
+                                                            const int64_t* __restrict__ rst,
+                                                            const int32_t* __restrict__ col_idx,
+                                                            const double* __restrict__ val,
+                                                            const int32_t* __restrict__ off,
+                                                            int32_t* __restrict__ ecol, double* __restrict__ eval) {
   // 8 lanes per entry: each quarter-warp copies one row's run with contiguous
   // (coalesced) loads and stores, 4 entries per warp instruction
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t t = gt >> 3;
   const int j = (int)(gt & 7);
   if (t >= N) return;
-  const int r = brow[t];
   const bool neg = bsg[t] < 0;
-  const int64_t rs = row_ptr[r];
-  const int len = (int)(row_ptr[r + 1] - rs);
+  const int64_t rs = rst[t];
   const int o = off[t];
+  const int len = off[t + 1] - o;
   for (int k = j; k < len; k += 8) {
     const int c = col_idx[rs + k];
     const double x = val[rs + k];
@@ -180,7 +188,8 @@ __global__ void __launch_bounds__(kThreads, 3) csr_reduce_kernel(
 size_t csr_ws_bytes(int64_t nrows, int s, int64_t nnz) {
   const int64_t N = nrows * (int64_t)s;
   const int64_t nexp = nnz * (int64_t)s;
-  return align_up(sizeof(int32_t) * (size_t)(N + 1)) + align_up(sizeof(int32_t) * (size_t)scan_scratch_ints(N + 1)) +
+  return align_up(sizeof(int32_t) * (size_t)(N + 1)) + align_up(sizeof(int64_t) * (size_t)std::max<int64_t>(N, 1)) +
+         align_up(sizeof(int32_t) * (size_t)scan_scratch_ints(N + 1)) +
          align_up(sizeof(double) * (size_t)std::max<int64_t>(nexp, 1)) +
          align_up(sizeof(int32_t) * (size_t)std::max<int64_t>(nexp, 1));
 }
@@ -191,13 +200,13 @@ int launch_gather_csr(int64_t m, int s, const int32_t* ptr, const int32_t* rows,
   const int64_t N = nrows * (int64_t)s;
   CsrWs w = csr_carve(ws, N, nnz * (int64_t)s);
   int rc;
-  csr_len_kernel<<<(unsigned)((N + 1 + 255) / 256), 256, 0, st>>>(N, rows, row_ptr, w.off);
+  csr_len_kernel<<<(unsigned)((N + 1 + 255) / 256), 256, 0, st>>>(N, rows, row_ptr, w.off, w.rst);
   note_launch();
   rc = launch_excl_scan_i32(w.off, N + 1, w.bs, st);
   if (rc) return rc;
   if (N > 0) {
-    csr_expand_kernel<<<(unsigned)((N * 8 + 255) / 256), 256, 0, st>>>(N, rows, sg, row_ptr, col_idx, val, w.off,
-                                                                        w.ecol, w.eval);
+    csr_expand_kernel<<<(unsigned)((N * 8 + 255) / 256), 256, 0, st>>>(N, sg, w.rst, col_idx, val, w.off, w.ecol,
+                                                                        w.eval);
     note_launch();
   }
   const int tile = (int)(d < kTileMax ? d : kTileMax);
