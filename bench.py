@@ -147,9 +147,14 @@ METRIC = "sketch GB/s of A streamed (S.A, S.H.D.A) & % HBM peak"
 
 
 # ---------------------------------------------------------------- GPU arm, one GPU
-def build_step(cfg, torch, layout="row"):
+def build_step(cfg, torch, layout="row", sketch="hashing"):
     from paper_2105_11815_b200 import pipeline
     from synth import device
+    var = sketch == "variant"
+    if sketch in ("dht", "srdht"):
+        A = device.dense(cfg)
+        b = device.rhs(cfg)
+        return pipeline.DhtStep(cfg.seed, A, b, cfg.m, cfg.s, sampling=sketch == "srdht", record=True), (A, b)
     if layout == "col" and cfg.kind != "csr":
         At = device.dense_colmajor(cfg)
         b = device.rhs(cfg)
@@ -157,11 +162,11 @@ def build_step(cfg, torch, layout="row"):
     if cfg.kind == "csr":
         rp, ci, v = device.csr(cfg)
         b = device.rhs(cfg)
-        return pipeline.CsrStep(cfg.seed, rp, ci, v, cfg.d, b, cfg.m, cfg.s, record=True), (rp, ci, v, b)
+        return pipeline.CsrStep(cfg.seed, rp, ci, v, cfg.d, b, cfg.m, cfg.s, record=True, variant=var), (rp, ci, v, b)
     A = device.dense(cfg)
     b = device.rhs(cfg)
     cls = pipeline.HrhtStep if cfg.hd else pipeline.PlainStep
-    return cls(cfg.seed, A, b, cfg.m, cfg.s, record=True), (A, b)
+    return cls(cfg.seed, A, b, cfg.m, cfg.s, record=True, variant=var), (A, b)
 
 
 def e2e_measure(cfg, inputs, steps, torch, layout="row"):
@@ -207,8 +212,23 @@ def e2e_measure(cfg, inputs, steps, torch, layout="row"):
                     "skh_rht_dense_host" if cfg.hd else "skh_sketch_dense_host")}
 
 
-def roofline(cfg, step, stage_ms, peak_gbs, peak_src, layout="row"):
+def roofline(cfg, step, stage_ms, peak_gbs, peak_src, layout="row", sketch="hashing"):
     """Dominant kernel and its algorithmic bytes per launch."""
+    if sketch in ("dht", "srdht"):
+        # stages of skh_hrdht_dense / skh_srdht_dense (row-major): D (+ transpose)
+        # reads A and writes a column-major copy, cuFFT D2Z (a library FFT)
+        # reads it and writes n/2+1 complex, the Hartley combine reads those and
+        # writes the row-major transform, the gather (or row sampling) reads it
+        nb = cfg.n * (cfg.d + 1) * 8
+        alg = {"diag": 2 * nb, "fft": 2 * nb, "hartley": 2 * nb,
+               "gather": nb + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5}
+        name = max((k for k in stage_ms if k in alg), key=lambda k: stage_ms[k])
+        t = stage_ms[name]
+        ach = alg[name] / (t / 1e3) / 1e9
+        return {"bound": "hbm", "kernel": ("cufft D2Z (library)" if name == "fft" else name), "achieved": round(ach, 1),
+                "peak": peak_gbs, "unit": "GB/s", "frac": round(ach / peak_gbs, 4), "traffic": None,
+                "traffic_source": None, "alg_bytes_per_launch": alg[name], "ms_per_launch": round(t, 4),
+                "peak_source": peak_src}
     if layout == "col":
         # dominant by time; algorithmic bytes of each kernel per launch:
         #  pass1: read + write (d + 1) columns of n_pad rows once
@@ -266,7 +286,7 @@ def gpu_arm_single(args, cfg):
 
     import paper_2105_11815_b200 as skh
     torch.cuda.set_device(0)
-    step, inputs = build_step(cfg, torch, args.layout)
+    step, inputs = build_step(cfg, torch, args.layout, args.sketch)
     torch.cuda.synchronize()
     for _ in range(max(args.warmup, 0)):
         step.run()
@@ -300,16 +320,19 @@ def gpu_arm_single(args, cfg):
                        "parallelism": "single GPU", "note": cfg.note},
             "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
             "gpu_launches": int(launches), "clocks": clocks}
-    line["roofline"] = roofline(cfg, step, stage_ms, pk["hbm_gbs"], src, args.layout)
+    line["roofline"] = roofline(cfg, step, stage_ms, pk["hbm_gbs"], src, args.layout, args.sketch)
+    if args.sketch != "hashing":
+        line["config"]["sketch"] = {"variant": "s-hashing variant (Def. 7)", "dht": "HR-DHT S_h F D (eq. (6.1))",
+                                    "srdht": "SR-DHT S_s F D (eq. (7.2))"}[args.sketch]
     del step
     if not args.no_e2e:
-        line["e2e"] = e2e_measure(cfg, inputs, args.e2e_steps, torch, args.layout)
+        line["e2e"] = e2e_measure(cfg, inputs, args.e2e_steps, torch, args.layout) if args.sketch == "hashing" else None
     del inputs
     torch.cuda.empty_cache()
-    if args.layout == "row" and cfg.kind != "csr" and cfg.hd and not args.no_alt_layout:
+    if args.layout == "row" and cfg.kind != "csr" and cfg.hd and args.sketch == "hashing" and not args.no_alt_layout:
         line["column_major"] = alt_layout_measure(args, cfg, torch, pk, src)
         torch.cuda.empty_cache()
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and args.sketch == "hashing":
         line["cpu_baseline"] = cpu_baseline(cfg)
     print(json.dumps(line), flush=True)
 
@@ -352,6 +375,9 @@ def main():
                     help="storage of dense A: row-major (default) or column-major (the paper's LAPACK layout)")
     ap.add_argument("--impl", default="skh", choices=["skh", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--sketch", default="hashing", choices=["hashing", "variant", "dht", "srdht"],
+                    help="hashing (default, Def. 4 / HRHT), the s-hashing variant (Def. 7), HR-DHT (eq. 6.1) "
+                         "or SR-DHT (eq. 7.2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt-layout", action="store_true",
                     help="skip the column-major measurement reported beside a row-major H D workload")

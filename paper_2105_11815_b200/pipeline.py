@@ -45,10 +45,12 @@ class _Timed:
 
 
 class HrhtStep:
-    """SA = S_h H D A, Sb = S_h H D b for a row-major A resident on the device."""
+    """SA = S_h H D A, Sb = S_h H D b for a row-major A resident on the device
+    (variant=True: S_h is the s-hashing variant of Def. 7)."""
 
-    def __init__(self, seed, A, b, m, s, record=False):
+    def __init__(self, seed, A, b, m, s, record=False, variant=False):
         self.seed, self.m, self.s = seed, int(m), int(s)
+        self.variant = bool(variant)
         self.A, self.b = A, b
         n, d = A.shape
         self.n, self.d = n, d
@@ -79,7 +81,7 @@ class HrhtStep:
     def run(self, timer=None):
         t = timer or self.timer
         t.start()
-        self.bl = api.hash_gen(self.seed, self.m, self.s, self.n_pad, out=self.bl)
+        self.bl = api.hash_gen(self.seed, self.m, self.s, self.n_pad, out=self.bl, variant=self.variant)
         t.mark()
         lo = 0
         for p, k in enumerate(self.plan):
@@ -99,10 +101,11 @@ class HrhtStep:
 
 
 class PlainStep:
-    """SA = S A, Sb = S b (s-hashing, no transform)."""
+    """SA = S A, Sb = S b (s-hashing, no transform; variant=True: Def. 7)."""
 
-    def __init__(self, seed, A, b, m, s, record=False):
+    def __init__(self, seed, A, b, m, s, record=False, variant=False):
         self.seed, self.m, self.s = seed, int(m), int(s)
+        self.variant = bool(variant)
         self.A, self.b = A, b
         n, d = A.shape
         dev = A.device
@@ -117,7 +120,7 @@ class PlainStep:
     def run(self, timer=None):
         t = timer or self.timer
         t.start()
-        self.bl = api.hash_gen(self.seed, self.m, self.s, self.A.shape[0], out=self.bl)
+        self.bl = api.hash_gen(self.seed, self.m, self.s, self.A.shape[0], out=self.bl, variant=self.variant)
         t.mark()
         api.sketch_dense(self.bl, self.A, self.b, SA=self.SA, Sb=self.Sb)
         t.mark()
@@ -125,10 +128,11 @@ class PlainStep:
 
 
 class CsrStep:
-    """Dense SA = S A, Sb = S b for CSR A."""
+    """Dense SA = S A, Sb = S b for CSR A (variant=True: Def. 7)."""
 
-    def __init__(self, seed, row_ptr, col_idx, val, d, b, m, s, record=False):
+    def __init__(self, seed, row_ptr, col_idx, val, d, b, m, s, record=False, variant=False):
         self.seed, self.m, self.s, self.d = seed, int(m), int(s), int(d)
+        self.variant = bool(variant)
         self.csr = (row_ptr, col_idx, val)
         self.b = b
         dev = row_ptr.device
@@ -145,7 +149,7 @@ class CsrStep:
         t = timer or self.timer
         t.start()
         n = self.csr[0].numel() - 1
-        self.bl = api.hash_gen(self.seed, self.m, self.s, n, out=self.bl)
+        self.bl = api.hash_gen(self.seed, self.m, self.s, n, out=self.bl, variant=self.variant)
         t.mark()
         api.sketch_csr(self.bl, *self.csr, self.d, self.b, SA=self.SA, Sb=self.Sb, ws=self.ws)
         t.mark()
@@ -188,3 +192,34 @@ class ColStep:
             return self.op(self.seed, self.At, self.b, SAt=self.SAt, Sb=self.Sb)
         return api.sketch_dense_colmajor(self.seed, self.At, self.b, self.m, self.s, SAt=self.SAt, Sb=self.Sb,
                                          ws=self.ws)
+
+
+class DhtStep:
+    """HR-DHT S_h F D (eq. (6.1)) or SR-DHT S_s F D (eq. (7.2)), row-major A: one
+    composite call, stages from the library's trace."""
+
+    def __init__(self, seed, A, b, m, s, sampling=False, record=False):
+        self.seed, self.m, self.s, self.sampling = seed, int(m), int(s), bool(sampling)
+        self.A, self.b = A, b
+        n, d = A.shape
+        dev = A.device
+        lib = api._lib.load()
+        nb = (lib.skh_srdht_dense_workspace_bytes(n, self.m, d) if sampling
+              else lib.skh_hrdht_dense_workspace_bytes(n, self.m, self.s, d))
+        self.ws = api._workspace(nb, dev)
+        self.SA = torch.empty(self.m, d, dtype=torch.float64, device=dev)
+        self.Sb = torch.empty(self.m, dtype=torch.float64, device=dev) if b is not None else None
+
+    def new_timer(self):
+        return api.Trace(16)
+
+    def run(self, timer=None):
+        if timer is None:
+            return self._call()
+        with timer:
+            return self._call()
+
+    def _call(self):
+        if self.sampling:
+            return api.srdht_dense(self.seed, self.A, self.b, self.m, SA=self.SA, Sb=self.Sb, ws=self.ws)
+        return api.hrdht_dense(self.seed, self.A, self.b, self.m, self.s, SA=self.SA, Sb=self.Sb, ws=self.ws)
