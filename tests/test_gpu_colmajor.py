@@ -244,3 +244,25 @@ def test_trace_stage_events():
     assert tr.names == ["begin", "hash_gen", "tile_lists", "pass1", "pass2_gather"]
     ms = tr.durations_ms()
     assert all(v >= 0 for v in ms.values())
+
+
+def test_determinism_stress_shared_memory_paths():
+    """compute-sanitizer is not available on this pool (SURVEY §5 asks for
+    racecheck); the kernels use no floating-point atomics, so a shared-memory
+    race would show up as run-to-run differences: five reruns of every
+    scatter-style path must be bitwise equal."""
+    from synth import configs, device, gen
+    cfg = configs.C2.scaled(n=1 << 15, d=33, m=300)
+    At = device.dense_colmajor(cfg)
+    b = device.rhs(cfg)
+    runs = [skh().rht_dense_colmajor(cfg.seed, At, b, cfg.m, 2) for _ in range(5)]
+    runs2 = [skh().sketch_dense_colmajor(cfg.seed, At, b, cfg.m, 3) for _ in range(5)]
+    c4 = configs.C4.scaled(n=20000, d=500, m=100)
+    rp, ci, v = (torch.from_numpy(x).cuda() for x in gen.csr(c4))
+    bl = skh().hash_gen(c4.seed, c4.m, c4.s, c4.n)
+    runs3 = [skh().sketch_csr(bl, rp, ci, v, c4.d) for _ in range(5)]
+    for rr in (runs, runs2, runs3):
+        for SA, Sb in rr[1:]:
+            assert torch.equal(SA, rr[0][0])
+            if Sb is not None:
+                assert torch.equal(Sb, rr[0][1])
