@@ -307,7 +307,8 @@ int skh_rht_colmajor(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0,
  *   skh_hrdht_dense_colmajor: A column-major (lda >= n), SA column-major (ldsa >= m),
  *                             s <= 8, m <= 65536
  * b nullable, Sb required iff b.  ws: the matching query (holds two transformed
- * copies of [A b]; creating the cuFFT plan needs the device). */
+ * copies of [A b]; creating the cuFFT plan needs the device).  cuFFT plans are
+ * cached per host thread, device, n and batch for the life of the process. */
 size_t skh_hrdht_dense_workspace_bytes(int64_t n, int64_t m, int32_t s, int64_t d);
 int skh_hrdht_dense(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d,
                     const double* A, int64_t lda, const double* b,
@@ -348,7 +349,11 @@ int skh_srdht_dense(uint64_t seed, int64_t n, int64_t m, int64_t d,
  * ||A x_s - b||).  m >= d.  Each LSQR iteration streams A twice through the
  * library's HBM kernels; the scalar recurrence runs on the host, so this call
  * SYNCHRONISES `stream` (twice per iteration) and returns when x is ready.
- * Deterministic: fixed-order reductions.  ws: skh_lls_workspace_bytes. */
+ * Deterministic: fixed-order reductions.  ws: skh_lls_workspace_bytes (it
+ * creates the per-thread cuSOLVER/cuBLAS handles, so it needs the device).
+ * Errors: argument errors as usual (nothing enqueued); a rank-deficient SA
+ * (some r_qq == 0) is detected after Step 2 and returns SKH_EINVAL with the
+ * workspace already written and x untouched. */
 size_t skh_lls_workspace_bytes(int64_t n, int64_t d, int64_t m);
 int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const double* b,
                   int64_t m, const double* SA, int64_t ldsa, const double* Sb,
