@@ -347,8 +347,9 @@ int skh_srdht_dense(uint64_t seed, int64_t n, int64_t m, int64_t d,
  * Outputs: x [d] (device), x_s [d] (device, nullable), info[2] (host:
  * step, LSQR iterations), stats[3] (host: final (7.1) estimate, ||r|| estimate,
  * ||A x_s - b||).  m >= d.  Each LSQR iteration streams A twice through the
- * library's HBM kernels; the scalar recurrence runs on the host, so this call
- * SYNCHRONISES `stream` (twice per iteration) and returns when x is ready.
+ * library's HBM kernels; the loop runs as one CUDA-graph launch with the scalar
+ * recurrence on the device (a host-driven loop is the fallback).  This call
+ * SYNCHRONISES `stream` and returns when x is ready.
  * Deterministic: fixed-order reductions.  ws: skh_lls_workspace_bytes (it
  * creates the per-thread cuSOLVER/cuBLAS handles, so it needs the device).
  * Errors: argument errors as usual (nothing enqueued); a rank-deficient SA

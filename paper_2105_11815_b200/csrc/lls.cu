@@ -10,8 +10,9 @@
 //          (7.1) estimate ||W^T r|| / (||W|| ||r||) <= tau_r (L1085-1089) or
 //          it_max.  Every iteration streams A twice -- u <- A (R^{-1} v) - alpha u
 //          and v <- R^{-T} (A^T u) - beta v -- through the two HBM-bound kernels
-//          below; the d x d triangular solves are cuBLAS dtrsv, the scalar
-//          recurrence runs on the host (two 8-byte read-backs per iteration).
+//          below; the d x d triangular solves are cuBLAS dtrsv; the whole loop
+//          is one CUDA-graph launch (WHILE conditional node, scalar recurrence
+//          on the device), with a host-driven loop as fallback.
 //  Step 5  x = R^{-1} y.
 //
 // Kernels (ours, deterministic: every reduction has a fixed order):
@@ -32,6 +33,7 @@
 #include <cusolverDn.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -51,8 +53,9 @@ template <bool SMEM>
 __global__ void __launch_bounds__(256) gemv_n_kernel(int64_t n, int64_t d, const double* __restrict__ A, int64_t lda,
                                                      const double* __restrict__ t, double beta,
                                                      const double* yin, double* out, double* __restrict__ sq,
-                                                     int64_t rows_per_cta) {
+                                                     int64_t rows_per_cta, const double* bdev) {
   extern __shared__ double ts[];
+  if (bdev) beta = *bdev;  // device-resident coefficient (graph-captured LSQR)
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   if (SMEM) {
     for (int64_t c = threadIdx.x; c < d; c += blockDim.x) ts[c] = t[c];
@@ -155,8 +158,9 @@ __global__ void colsum_kernel(int64_t nblk, int64_t d, const double* __restrict_
 template <bool SMEM>
 __global__ void __launch_bounds__(256) cm_av_kernel(int64_t n, int64_t d, const double* __restrict__ A, int64_t lda,
                                                     const double* __restrict__ t, double beta, const double* yin,
-                                                    double* out, double* __restrict__ sq) {
+                                                    double* out, double* __restrict__ sq, const double* bdev) {
   extern __shared__ double ts[];
+  if (bdev) beta = *bdev;
   if (SMEM) {
     for (int64_t c = threadIdx.x; c < d; c += blockDim.x) ts[c] = t[c];
     __syncthreads();
@@ -247,14 +251,20 @@ __global__ void sum_parts_kernel(int64_t np, const double* __restrict__ parts, d
   }
 }
 
-__global__ void scale_vec_kernel(int64_t n, double* x, double a) {
+__global__ void scale_vec_kernel(int64_t n, double* x, double a, const double* adev = nullptr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (adev) a = *adev;
   if (i < n) x[i] *= a;
 }
 
 // y += p * w;  w = v + q * w
-__global__ void lsqr_update_kernel(int64_t d, double* y, double* w, const double* v, double p, double q) {
+__global__ void lsqr_update_kernel(int64_t d, double* y, double* w, const double* v, double p, double q,
+                                   const double* pq = nullptr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pq) {
+    p = pq[0];
+    q = pq[1];
+  }
   if (i < d) {
     const double wi = w[i];
     y[i] = fma(p, wi, y[i]);
@@ -263,9 +273,61 @@ __global__ void lsqr_update_kernel(int64_t d, double* y, double* w, const double
 }
 
 // out = a * x + b * y
-__global__ void axpby_kernel(int64_t n, double a, const double* x, double b, const double* y, double* out) {
+__global__ void axpby_kernel(int64_t n, double a, const double* x, double b, const double* y, double* out,
+                             const double* bdev = nullptr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (bdev) b = *bdev;
   if (i < n) out[i] = y ? fma(b, y[i], a * x[i]) : a * x[i];
+}
+
+// ---- device-resident LSQR scalars (slots of LlsWs::scal)
+enum : int {
+  kSqBeta = 0, kSqAlpha = 1, kAlpha = 2, kBeta = 3, kRhobar = 4, kPhibar = 5, kAnorm2 = 6, kTest2 = 7,
+  kIters = 8, kP = 9, kQ = 10, kInvBeta = 11, kInvAlpha = 12, kNegAlpha = 13, kNegBeta = 14, kTau = 15,
+  kItMax = 16, kNumScal = 24
+};
+
+// beta = ||u||; u /= beta (when > 0); anorm2 += alpha^2 + beta^2 -- the host loop's order
+__global__ void lsqr_beta_kernel(double* sc) {
+  const double beta = sqrt(sc[kSqBeta]);
+  const double alpha = sc[kAlpha];
+  sc[kBeta] = beta;
+  sc[kInvBeta] = beta > 0.0 ? 1.0 / beta : 1.0;
+  sc[kNegBeta] = -beta;
+  sc[kAnorm2] = sc[kAnorm2] + alpha * alpha + beta * beta;
+}
+
+// alpha = ||v||; the plane rotation; the (7.1) estimate; the loop condition
+__global__ void lsqr_alpha_kernel(double* sc, cudaGraphConditionalHandle cond) {
+  const double alpha = sqrt(sc[kSqAlpha]);
+  const double beta = sc[kBeta];
+  sc[kAlpha] = alpha;
+  sc[kInvAlpha] = alpha > 0.0 ? 1.0 / alpha : 1.0;
+  sc[kNegAlpha] = -alpha;
+  const double rhobar = sc[kRhobar], phibar = sc[kPhibar];
+  const double rho = sqrt(rhobar * rhobar + beta * beta);
+  const double c = rhobar / rho, s = beta / rho;
+  const double theta = s * alpha;
+  sc[kRhobar] = -c * alpha;
+  const double phi = c * phibar;
+  const double nphibar = s * phibar;
+  sc[kPhibar] = nphibar;
+  sc[kP] = phi / rho;
+  sc[kQ] = -theta / rho;
+  const double arnorm = alpha * fabs(s * phi);
+  const double it = sc[kIters] + 1.0;
+  sc[kIters] = it;
+  bool done;
+  if (nphibar == 0.0) {
+    sc[kTest2] = 0.0;
+    done = true;
+  } else {
+    const double t2 = arnorm / (sqrt(sc[kAnorm2]) * nphibar);
+    sc[kTest2] = t2;
+    done = t2 <= sc[kTau];
+  }
+  done = done || it >= sc[kItMax];
+  cudaGraphSetConditional(cond, done ? 0u : 1u);
 }
 
 // row-major m x d (ld ldsa) -> column-major m x d (ld m)
@@ -326,7 +388,7 @@ struct LlsWs {
   double* xs;      // [d]
   double* part;    // gemv_t partials [nblk x d]
   double* sq;      // norm partials [max(nrb, nsq)]
-  double* scal;    // [8] device scalars
+  double* scal;    // [kNumScal] device scalars
   int* devinfo;
   double* lwork;   // cuSOLVER workspace
   int lwork_n;
@@ -364,7 +426,7 @@ LlsWs lls_layout(void* base, int64_t n, int64_t d, int64_t m, int lwork_n) {
   w.xs = (double*)take(sizeof(double) * (size_t)d);
   w.part = (double*)take(sizeof(double) * (size_t)std::max(w.nblk, nblk_cm) * d);
   w.sq = (double*)take(sizeof(double) * (size_t)nsq);
-  w.scal = (double*)take(sizeof(double) * 8);
+  w.scal = (double*)take(sizeof(double) * kNumScal);
   w.devinfo = (int*)take(sizeof(int) * 4);
   w.lwork = (double*)take(sizeof(double) * (size_t)std::max(lwork_n, 1));
   w.lwork_n = lwork_n;
@@ -389,16 +451,16 @@ int query_lwork(int64_t m, int64_t d, int* lw) {
 
 // out = A t + beta yin (row-major A); returns ||out||^2 through w.scal[slot] (device)
 int gemv_n(int64_t n, int64_t d, const double* A, int64_t lda, const double* t, double beta, const double* yin,
-           double* out, const LlsWs& w, int slot, cudaStream_t st) {
+           double* out, const LlsWs& w, int slot, cudaStream_t st, const double* bdev = nullptr) {
   const int64_t rows = 256;
   const int64_t grid = (n + rows - 1) / rows;
   if (d <= kMaxSmemX) {
     const size_t smem = sizeof(double) * (size_t)d;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(gemv_n_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    gemv_n_kernel<true><<<(unsigned)grid, 256, smem, st>>>(n, d, A, lda, t, beta, yin, out, w.sq, rows);
+    gemv_n_kernel<true><<<(unsigned)grid, 256, smem, st>>>(n, d, A, lda, t, beta, yin, out, w.sq, rows, bdev);
   } else {
-    gemv_n_kernel<false><<<(unsigned)grid, 256, 0, st>>>(n, d, A, lda, t, beta, yin, out, w.sq, rows);
+    gemv_n_kernel<false><<<(unsigned)grid, 256, 0, st>>>(n, d, A, lda, t, beta, yin, out, w.sq, rows, bdev);
   }
   note_launch();
   sum_parts_kernel<<<1, 32, 0, st>>>(grid, w.sq, w.scal + slot);
@@ -422,16 +484,17 @@ int sqnorm(int64_t n, const double* x, const LlsWs& w, int slot, cudaStream_t st
 
 // out = A t + beta yin and ||out||^2 -> scal[slot], for either layout
 int apply_A(bool cm, int64_t n, int64_t d, const double* A, int64_t lda, const double* t, double beta,
-            const double* yin, double* out, const LlsWs& w, int slot, cudaStream_t st) {
-  if (!cm) return gemv_n(n, d, A, lda, t, beta, yin, out, w, slot, st);
+            const double* yin, double* out, const LlsWs& w, int slot, cudaStream_t st,
+            const double* bdev = nullptr) {
+  if (!cm) return gemv_n(n, d, A, lda, t, beta, yin, out, w, slot, st, bdev);
   const int64_t grid = (n + 255) / 256;
   if (d <= kMaxSmemX) {
     const size_t smem = sizeof(double) * (size_t)d;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(cm_av_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cm_av_kernel<true><<<(unsigned)grid, 256, smem, st>>>(n, d, A, lda, t, beta, yin, out, w.sq);
+    cm_av_kernel<true><<<(unsigned)grid, 256, smem, st>>>(n, d, A, lda, t, beta, yin, out, w.sq, bdev);
   } else {
-    cm_av_kernel<false><<<(unsigned)grid, 256, 0, st>>>(n, d, A, lda, t, beta, yin, out, w.sq);
+    cm_av_kernel<false><<<(unsigned)grid, 256, 0, st>>>(n, d, A, lda, t, beta, yin, out, w.sq, bdev);
   }
   note_launch();
   sum_parts_kernel<<<1, 32, 0, st>>>(grid, w.sq, w.scal + slot);
@@ -474,6 +537,99 @@ int trsv(Handles* h, int64_t d, const LlsWs& w, int64_t m, bool trans, double* x
     set_error("lls: cublasDtrsv failed");
     return SKH_ECUDA;
   }
+  return SKH_OK;
+}
+
+// Step 4 as ONE graph launch: a WHILE conditional node whose body is one LSQR
+// iteration (the two HBM passes over A, the two triangular solves, the vector
+// updates and the scalar recurrence, all on the device); lsqr_alpha_kernel
+// clears the condition when (7.1) holds or it_max is reached.  No host round
+// trips inside the loop; the arithmetic is the host loop's, operation for
+// operation (IEEE sqrt and division on the device), so both give the same bits.
+// Returns SKH_OK with *ex instantiated, or an error (the caller then runs the
+// host loop; nothing has been enqueued on st).
+int lsqr_graph_build(Handles* h, bool cm, int64_t n, int64_t d, int64_t m, const double* A, int64_t lda,
+                     const LlsWs& w, cudaStream_t st, cudaGraphExec_t* ex) {
+  double* sc = w.scal;
+  cudaStream_t cs = nullptr;
+  cudaGraph_t g = nullptr;
+  *ex = nullptr;
+  auto fail = [&]() {
+    if (g) cudaGraphDestroy(g);
+    if (cs) cudaStreamDestroy(cs);
+    cublasSetStream(h->blas, st);
+    cudaGetLastError();
+    return SKH_ECUDA;
+  };
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess || cudaGraphCreate(&g, 0) != cudaSuccess)
+    return fail();
+  cudaGraphConditionalHandle cond;
+  if (cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) return fail();
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = cond;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, g, nullptr, 0, &np) != cudaSuccess) return fail();
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  if (cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return fail();
+  cublasSetStream(h->blas, cs);
+  int erc = SKH_OK;
+  {  // one iteration, exactly the host loop's operations
+    axpby_kernel<<<nblocks(d), 256, 0, cs>>>(d, 1.0, w.v, 0.0, nullptr, w.t);  // t = v
+    if (!erc) erc = trsv(h, d, w, m, false, w.t);
+    if (!erc) erc = apply_A(cm, n, d, A, lda, w.t, 0.0, w.u, w.u, w, kSqBeta, cs, sc + kNegAlpha);
+    lsqr_beta_kernel<<<1, 1, 0, cs>>>(sc);
+    scale_vec_kernel<<<nblocks(n), 256, 0, cs>>>(n, w.u, 1.0, sc + kInvBeta);
+    if (!erc) erc = apply_AT(cm, n, d, A, lda, w.u, 0.0, nullptr, w.t, w, cs);
+    if (!erc) erc = trsv(h, d, w, m, true, w.t);
+    axpby_kernel<<<nblocks(d), 256, 0, cs>>>(d, 1.0, w.t, 0.0, w.v, w.v, sc + kNegBeta);
+    if (!erc) erc = sqnorm(d, w.v, w, kSqAlpha, cs);
+    lsqr_alpha_kernel<<<1, 1, 0, cs>>>(sc, cond);
+    scale_vec_kernel<<<nblocks(d), 256, 0, cs>>>(d, w.v, 1.0, sc + kInvAlpha);
+    lsqr_update_kernel<<<nblocks(d), 256, 0, cs>>>(d, w.y, w.w, w.v, 0.0, 0.0, sc + kP);
+  }
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(cs, &captured);
+  cublasSetStream(h->blas, st);
+  if (erc || ce != cudaSuccess || cudaGraphInstantiate(ex, g, 0) != cudaSuccess) {
+    *ex = nullptr;
+    return fail();
+  }
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(cs);
+  return SKH_OK;
+}
+
+int lsqr_graph_run(cudaGraphExec_t ex, const LlsWs& w, double alpha, double beta, double tau_r, int64_t it_max,
+                   cudaStream_t st, int64_t* it_out, double* test2_out, double* phibar_out) {
+  double init[kNumScal] = {};
+  init[kAlpha] = alpha;
+  init[kBeta] = beta;
+  init[kRhobar] = alpha;
+  init[kPhibar] = beta;
+  init[kAnorm2] = 0.0;
+  init[kTest2] = INFINITY;
+  init[kIters] = 0.0;
+  init[kNegAlpha] = -alpha;
+  init[kTau] = tau_r;
+  init[kItMax] = (double)it_max;
+  double* sc = w.scal;
+  if (cudaMemcpyAsync(sc, init, sizeof(init), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return check_launch("lsqr graph: init");
+  if (cudaGraphLaunch(ex, st) != cudaSuccess) return check_launch("lsqr graph launch");
+  // kernels of the body, counted once per iteration after the fact
+  double out[kNumScal];
+  if (cudaMemcpyAsync(out, sc, sizeof(out), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return check_launch("lsqr graph: read-back");
+  *it_out = (int64_t)out[kIters];
+  *test2_out = out[kTest2];
+  *phibar_out = out[kPhibar];
+  for (int64_t i = 0; i < *it_out * 13; ++i) note_launch();
   return SKH_OK;
 }
 
@@ -590,7 +746,24 @@ static int lls_solve_impl(bool cm, int64_t n, int64_t d, const double* A, int64_
     if ((rc = sqnorm(d, w.v, w, 1, st)) || (rc = read_scal(w, 1, &alpha, st))) return rc;
     alpha = sqrt(alpha);
   }
-  if (beta > 0.0 && alpha > 0.0) {
+  const char* hl = getenv("SKH_LLS_HOSTLOOP");  // 1: the host-driven loop (reference for the graph's bits)
+  const bool host_loop = hl && atoi(hl) != 0;
+  bool graph_done = false;
+  if (beta > 0.0 && alpha > 0.0 && it_max > 0 && !host_loop) {
+    cudaGraphExec_t ex = nullptr;
+    if (lsqr_graph_build(h, cm, n, d, m, A, lda, w, st, &ex) == SKH_OK) {
+      scale_vec_kernel<<<nblocks(d), 256, 0, st>>>(d, w.v, 1.0 / alpha);
+      note_launch();
+      cudaMemcpyAsync(w.w, w.v, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);
+      rc = lsqr_graph_run(ex, w, alpha, beta, tau_r, it_max, st, &it, &test2, &phibar);
+      cudaGraphExecDestroy(ex);
+      if (rc) return rc;
+      graph_done = true;
+    }
+  }
+  if (graph_done) {
+    // LSQR ran entirely on the device (CUDA graph WHILE node)
+  } else if (beta > 0.0 && alpha > 0.0) {
     scale_vec_kernel<<<nblocks(d), 256, 0, st>>>(d, w.v, 1.0 / alpha);
     note_launch();
     cudaMemcpyAsync(w.w, w.v, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);

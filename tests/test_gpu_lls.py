@@ -196,3 +196,25 @@ def test_ski_lls_dense_composite(transform):
     best = np.linalg.norm(A @ xs - b)
     assert info["step"] == 4 and info["test2"] <= 1e-6
     assert np.linalg.norm(A @ np_(x) - b) <= best * (1 + 1e-10)
+
+
+@pytest.mark.parametrize("colmajor", [False, True])
+def test_lsqr_graph_equals_host_loop(colmajor, monkeypatch):
+    """Step 4 runs as one CUDA-graph WHILE loop with the scalar recurrence on the
+    device; SKH_LLS_HOSTLOOP=1 selects the host-driven loop.  Same IEEE
+    operations in the same order: bit-identical x, same iteration count."""
+    from oracle import sketch
+    A, b = ill_conditioned(6000, 48, 3, 1e4)
+    SA, Sb = sketch.sketch_dense(4, A, b, 150, 2)
+    if colmajor:
+        args = (torch.from_numpy(np.ascontiguousarray(A.T)).cuda(), torch.from_numpy(b).cuda(),
+                torch.from_numpy(np.ascontiguousarray(SA.T)).cuda(), torch.from_numpy(Sb).cuda())
+    else:
+        args = tuple(torch.from_numpy(x).cuda() for x in (A, b, SA, Sb))
+    solver = skh().LlsSolver(6000, 48, 150)
+    x1, i1 = solver(*args, colmajor=colmajor)
+    x1 = x1.clone()
+    monkeypatch.setenv("SKH_LLS_HOSTLOOP", "1")
+    x2, i2 = solver(*args, colmajor=colmajor)
+    assert i1 == i2 and i1["iters"] > 3
+    assert torch.equal(x1, x2)
