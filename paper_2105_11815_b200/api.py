@@ -358,9 +358,12 @@ def rht_colmajor(seed, Xt, nrows=None, row0=0, apply_diag=True, Yt=None):
     nrows = nvalid if nrows is None else int(nrows)
     if Yt is None:
         Yt = torch.empty(ncols, nrows, dtype=torch.float64, device=Xt.device)
-    rc = lib.skh_rht_colmajor(int(seed) & (2**64 - 1), nrows, nvalid, int(row0), ncols, _ptr(Xt),
-                              max(Xt.stride(0), nvalid), _ptr(Yt), max(Yt.stride(0), nrows), int(bool(apply_diag)),
-                              _stream())
+    ldx = _ld_cm(Xt, nvalid) if ncols > 1 else max(Xt.stride(0), nvalid)
+    ldy = _ld_cm(Yt, nrows) if ncols > 1 else max(Yt.stride(0), nrows)
+    if Xt.stride(-1) != 1 or Yt.stride(-1) != 1:
+        raise ValueError("rht_colmajor: columns must be contiguous (unit last stride)")
+    rc = lib.skh_rht_colmajor(int(seed) & (2**64 - 1), nrows, nvalid, int(row0), ncols, _ptr(Xt), ldx, _ptr(Yt),
+                              ldy, int(bool(apply_diag)), _stream())
     _lib.check(rc, "skh_rht_colmajor")
     return Yt
 
