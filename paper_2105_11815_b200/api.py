@@ -33,9 +33,10 @@ def _need_cuda(*ts):
 
 
 def _ld(t):
-    if t.dim() != 2 or t.stride(1) != 1:
+    # a size-1 dimension's stride is arbitrary in torch/numpy: ignore it
+    if t.dim() != 2 or (t.stride(1) != 1 and t.size(1) > 1):
         raise ValueError("expected a row-major 2-D tensor with unit column stride")
-    return t.stride(0)
+    return t.stride(0) if t.size(0) > 1 else max(t.size(1), 1)
 
 
 def _workspace(nbytes, device):
@@ -277,7 +278,9 @@ def ordered_sum(parts, alpha=1.0, out=None):
 # lda = At.stride(0); SA comes back the same way, as a (d, m) tensor = SA^T.
 
 def _ld_cm(t, rows):
-    if t.dim() != 2 or t.stride(1) != 1 or t.stride(0) < rows:
+    if t.dim() == 2 and t.size(0) <= 1 and (t.stride(1) == 1 or t.size(1) <= 1):
+        return max(rows, 1)                  # one column: its leading stride is never used
+    if t.dim() != 2 or (t.stride(1) != 1 and t.size(1) > 1) or t.stride(0) < rows:
         raise ValueError("expected a (cols, rows) tensor with unit last stride (column-major storage)")
     return t.stride(0)
 
