@@ -215,12 +215,14 @@ def e2e_measure(cfg, inputs, steps, torch, layout="row"):
 def roofline(cfg, step, stage_ms, peak_gbs, peak_src, layout="row", sketch="hashing"):
     """Dominant kernel and its algorithmic bytes per launch."""
     if sketch in ("dht", "srdht"):
-        # stages of skh_hrdht_dense / skh_srdht_dense (row-major): D (+ transpose)
-        # reads A and writes a column-major copy, cuFFT D2Z (a library FFT)
-        # reads it and writes n/2+1 complex, the Hartley combine reads those and
-        # writes the row-major transform, the gather (or row sampling) reads it
+        # stages of skh_hrdht_dense / skh_srdht_dense (row-major).  n = 2^L
+        # (csrc/fht.cu): pass A reads D [A | b] and writes the half spectrum
+        # (n/2 + n1 complex per column ~ the same bytes), pass B reads it and
+        # writes the row-major transform.  Other n (or SKH_DHT_CUFFT=1): D +
+        # transpose, cuFFT D2Z (a library FFT), Hartley combine + transpose.
+        # Then the gather (or row sampling) reads the transform once.
         nb = cfg.n * (cfg.d + 1) * 8
-        alg = {"diag": 2 * nb, "fft": 2 * nb, "hartley": 2 * nb,
+        alg = {"diag": 2 * nb, "fft": 2 * nb, "hartley": 2 * nb, "dht_passA": 2 * nb, "dht_passB": 2 * nb,
                "gather": nb + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5}
         name = max((k for k in stage_ms if k in alg), key=lambda k: stage_ms[k])
         t = stage_ms[name]

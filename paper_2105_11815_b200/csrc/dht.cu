@@ -17,6 +17,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <map>
 #include <tuple>
@@ -33,7 +35,23 @@ int launch_cm_gather(const double* X, int64_t ldx, int64_t ncolX, const double* 
                      int lo, int K2, const void* lists_ws, int s, int64_t m, double* SA, int64_t ldsa,
                      int64_t ncolSA, double* Sb, double alpha, cudaStream_t st);
 
+// fht.cu (n = 2^L, row-major: our own two-pass Hartley transform)
+bool dht_pow2_supported(int64_t n);
+size_t dht_pow2_z_elems(int64_t n, int64_t ncol);
+int launch_dht_pow2(int64_t n, int64_t d, const double* A, int64_t lda, const double* b, uint64_t dkey,
+                    double2* Z, double2* tw, double* H, int64_t ldh, double* hb, cudaStream_t st);
+
 namespace {
+
+// Row-major A with n = 2^L (4 <= n <= 2^18) takes the fht.cu passes unless
+// SKH_DHT_CUFFT=1 (kept for comparison: D + transpose, cuFFT D2Z, transpose).
+bool use_pow2(int64_t n, bool rowmajor) {
+  static const bool force_cufft = [] {
+    const char* e = getenv("SKH_DHT_CUFFT");
+    return e && e[0] == '1';
+  }();
+  return rowmajor && !force_cufft && dht_pow2_supported(n);
+}
 
 __device__ __forceinline__ double dsign(uint64_t dkey, int64_t g) {
   return ((stream_u(dkey, (uint64_t)(g >> 6)) >> (g & 63)) & 1ull) ? -1.0 : 1.0;
@@ -147,7 +165,8 @@ int get_plan(int64_t n, int64_t ncol, Plan** out) {
 
 struct DhtWs {
   double* Y;                 // [ncol][n] D A, then Fhat D A (column-major)
-  cufftDoubleComplex* Z;     // [ncol][n/2 + 1]
+  cufftDoubleComplex* Z;     // [ncol][n/2 + 1] (cuFFT) or fht.cu's four-step buffer
+  cufftDoubleComplex* tw;    // fht.cu: W_n^e, e <= n/2
   double* H;                 // row-major Fhat D A [n][d] (row-major path)
   double* hb;                // Fhat D b [n] (row-major path)
   void* fftwork;
@@ -163,6 +182,7 @@ struct DhtWs {
 
 DhtWs dht_layout(void* base, int64_t n, int64_t m, int s, int64_t d, bool rowmajor, size_t fftwork) {
   DhtWs w{};
+  const bool pow2 = use_pow2(n, rowmajor);
   char* p = static_cast<char*>(base);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -171,13 +191,18 @@ DhtWs dht_layout(void* base, int64_t n, int64_t m, int s, int64_t d, bool rowmaj
     return q;
   };
   const int64_t ncol = d + 1;
-  w.Y = (double*)take(sizeof(double) * (size_t)n * ncol);
-  w.Z = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * (size_t)(n / 2 + 1) * ncol);
+  if (pow2) {
+    w.Z = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * dht_pow2_z_elems(n, ncol));
+    w.tw = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * (size_t)(n / 2 + 1));
+  } else {
+    w.Y = (double*)take(sizeof(double) * (size_t)n * ncol);
+    w.Z = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * (size_t)(n / 2 + 1) * ncol);
+  }
   if (rowmajor) {
     w.H = (double*)take(sizeof(double) * (size_t)n * d);
     w.hb = (double*)take(sizeof(double) * (size_t)n);
   }
-  w.fftwork = take(std::max<size_t>(fftwork, 16));
+  if (!pow2) w.fftwork = take(std::max<size_t>(fftwork, 16));
   w.col_rows = (int32_t*)take(sizeof(int32_t) * (size_t)n * s);
   w.col_signs = (int8_t*)take((size_t)n * s);
   w.ptr = (int32_t*)take(sizeof(int32_t) * (size_t)(m + 1));
@@ -207,9 +232,27 @@ int check_args(int64_t n, int64_t m, int32_t s, int64_t d, bool rowmajor) {
 
 size_t ws_bytes_for(int64_t n, int64_t m, int32_t s, int64_t d, bool rowmajor) {
   if (check_args(n, m, s, d, rowmajor)) return 0;
+  if (use_pow2(n, rowmajor)) return dht_layout(nullptr, n, m, s, d, rowmajor, 0).total;
   Plan* p = nullptr;
   if (get_plan(n, d + 1, &p)) return 0;
   return dht_layout(nullptr, n, m, s, d, rowmajor, p->work).total;
+}
+
+// row-major H = Fhat D A, hb = Fhat D b in the workspace: S_h (or S_s) applied
+int finish_rowmajor(uint64_t seed, int64_t n, int64_t m, int64_t d, const DhtWs& w, const double* b, double* SA,
+                    int64_t ldsa, double* Sb, double c, bool sample, cudaStream_t st) {
+  int rc;
+  if (sample) {
+    sample_rows_kernel<<<(unsigned)m, 256, 0, st>>>(m, n, d, mix64(seed ^ 0x53414D50ull), w.H, w.hb, SA, ldsa,
+                                                    b ? Sb : nullptr, 1.0 / sqrt((double)n));
+    note_launch();
+    if ((rc = check_launch("srdht: sample"))) return rc;
+  } else {
+    if ((rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.H, d, SA, ldsa, c, st))) return rc;
+    if (b && (rc = launch_gather_vec(m, w.ptr, w.rows, w.signs, w.hb, Sb, c, st))) return rc;
+  }
+  skh_trace_mark(st, "gather");
+  return SKH_OK;
 }
 
 int hrdht_run(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const double* A, int64_t lda,
@@ -226,12 +269,15 @@ int hrdht_run(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const d
     return SKH_EDIM;
   }
   const int64_t ncol = d + (b ? 1 : 0);
+  const bool pow2 = use_pow2(n, rowmajor);
   Plan* plan = nullptr;
-  if ((rc = get_plan(n, ncol, &plan))) return rc;
-  // the workspace query sizes the FFT for d + 1 columns, the largest plan
   Plan* pmax = nullptr;
-  if ((rc = get_plan(n, d + 1, &pmax))) return rc;
-  const DhtWs w = dht_layout(ws, n, m, s, d, rowmajor, std::max(plan->work, pmax->work));
+  if (!pow2) {
+    if ((rc = get_plan(n, ncol, &plan))) return rc;
+    // the workspace query sizes the FFT for d + 1 columns, the largest plan
+    if ((rc = get_plan(n, d + 1, &pmax))) return rc;
+  }
+  const DhtWs w = dht_layout(ws, n, m, s, d, rowmajor, pow2 ? 0 : std::max(plan->work, pmax->work));
   if (!ws || ws_bytes < w.total) {
     set_error("hrdht workspace too small: need %zu bytes", w.total);
     return SKH_EWORKSPACE;
@@ -246,6 +292,11 @@ int hrdht_run(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const d
     return rc;
   skh_trace_mark(st, "hash_gen");
   const uint64_t dkey = key_diag(seed);
+  const double c = 1.0 / sqrt((double)n * (double)s);
+  if (pow2) {
+    if ((rc = launch_dht_pow2(n, d, A, lda, b, dkey, (double2*)w.Z, (double2*)w.tw, w.H, d, w.hb, st))) return rc;
+    return finish_rowmajor(seed, n, m, d, w, b, SA, ldsa, Sb, c, sample, st);
+  }
   if (rowmajor) {
     dim3 grid((unsigned)((d + 31) / 32), (unsigned)((n + 31) / 32));
     diag_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(n, d, A, lda, w.Y, dkey);
@@ -267,22 +318,13 @@ int hrdht_run(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const d
     return SKH_ECUDA;
   }
   skh_trace_mark(st, "fft");
-  const double c = 1.0 / sqrt((double)n * (double)s);
   if (rowmajor) {
     dim3 grid((unsigned)((ncol + 31) / 32), (unsigned)((n + 31) / 32));
     hartley_rm_kernel<<<grid, dim3(32, 8), 0, st>>>(n, d, w.Z, w.H, b ? w.hb : nullptr);
     note_launch();
     if ((rc = check_launch("hrdht: hartley"))) return rc;
     skh_trace_mark(st, "hartley");
-    if (sample) {
-      sample_rows_kernel<<<(unsigned)m, 256, 0, st>>>(m, n, d, mix64(seed ^ 0x53414D50ull), w.H, w.hb, SA, ldsa,
-                                                      b ? Sb : nullptr, 1.0 / sqrt((double)n));
-      note_launch();
-      if ((rc = check_launch("srdht: sample"))) return rc;
-    } else {
-      if ((rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.H, d, SA, ldsa, c, st))) return rc;
-      if (b && (rc = launch_gather_vec(m, w.ptr, w.rows, w.signs, w.hb, Sb, c, st))) return rc;
-    }
+    return finish_rowmajor(seed, n, m, d, w, b, SA, ldsa, Sb, c, sample, st);
   } else {
     hartley_cm_kernel<<<(unsigned)((n * ncol + 255) / 256), 256, 0, st>>>(n, ncol, w.Z, w.Y);
     note_launch();

@@ -34,9 +34,13 @@ def rel(a, b):
 
 CASES = [(1, 1, 1, 1), (2, 3, 2, 1), (7, 2, 5, 2), (100, 17, 16, 2), (1000, 64, 112, 1), (4097, 33, 200, 3),
          (65536, 8, 448, 1), (100003, 3, 1000, 2)]
+# n = 2^L, 2 <= L <= 18, row-major: the two-pass transform of csrc/fht.cu (every
+# tile size 2..512, column tiles 8/16 with ragged tails, the 2^19 cuFFT fallback)
+POW2 = [(4, 1, 2, 1), (8, 15, 4, 2), (16, 16, 8, 1), (32, 17, 8, 3), (512, 33, 64, 2), (1024, 7, 100, 1),
+        (4096, 40, 300, 2), (1 << 17, 9, 700, 2), (1 << 18, 5, 800, 1), (1 << 19, 2, 900, 1)]
 
 
-@pytest.mark.parametrize("n,d,m,s", CASES)
+@pytest.mark.parametrize("n,d,m,s", CASES + POW2)
 def test_hrdht_rowmajor(n, d, m, s):
     from oracle import hartley
     r = np.random.default_rng(n + d)
@@ -59,9 +63,10 @@ def test_hrdht_colmajor(n, d, m, s):
     assert rel(np_(SAt).T, SAo) <= TOL and rel(np_(Sb), Sbo) <= TOL
 
 
-def test_hrdht_no_b_deterministic_and_padded_ld():
+@pytest.mark.parametrize("n", [3000, 4096])
+def test_hrdht_no_b_deterministic_and_padded_ld(n):
     from oracle import hartley
-    n, d, m, s = 3000, 5, 64, 2
+    d, m, s = 5, 64, 2
     A = np.random.default_rng(3).standard_normal((n, d))
     buf = torch.zeros(n, d + 3, dtype=torch.float64, device="cuda")
     buf[:, :d] = torch.from_numpy(A)
@@ -87,7 +92,8 @@ def test_hrdht_C2_full_sampled_columns():
     assert rel(np_(Sb), Sbo) <= TOL
 
 
-@pytest.mark.parametrize("n,d,m", [(1, 1, 1), (100, 7, 30), (4000, 40, 700), (4097, 3, 5), (30000, 16, 50)])
+@pytest.mark.parametrize("n,d,m", [(1, 1, 1), (100, 7, 30), (4000, 40, 700), (4097, 3, 5), (30000, 16, 50),
+                                   (8192, 20, 100)])
 def test_srdht(n, d, m):
     """SR-DHT (eq. (7.2)) vs oracle/sampling.py."""
     from oracle import sampling
