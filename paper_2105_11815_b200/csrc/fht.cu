@@ -51,59 +51,88 @@ __global__ void twiddle_kernel(int64_t n, double2* __restrict__ tw) {
 __device__ __forceinline__ int bitrev(int i, int K) { return (int)(__brev((unsigned)i) >> (32 - K)); }
 
 // One register round of the DIF FFT over index bits [P - a, P) of an N = 2^K
-// point transform, TC columns, z[i * TC + c].  FINAL: P - a == 0, the values are
-// handed to `epi(i, c, v)` instead of being written back.
-template <int K, int TC, int P, int A, bool FINAL, class Epi>
-__device__ __forceinline__ void dif_round(double2* __restrict__ z, const double2* __restrict__ wN, Epi&& epi) {
+// point transform, TC columns, z[i * TC + c].  FIRST: the inputs come from
+// `ld(i, c)` (global memory) instead of shared memory; FINAL: P - a == 0, the
+// outputs go to `epi(i, c, v)` instead of back to shared memory.  A thread takes
+// CH groups at a time (all their loads issued before any butterfly), CH * 2^a
+// <= 16 complex values in registers.
+template <int K, int TC, int P, int A, bool FIRST, bool FINAL, class Ld, class Epi>
+__device__ __forceinline__ void dif_round(double2* __restrict__ z, const double2* __restrict__ wN, Ld&& ld,
+                                          Epi&& epi) {
   constexpr int N = 1 << K, R = 1 << A, p = P - A;
   constexpr int G = (N >> A) * TC;
-  for (int g = threadIdx.x; g < G; g += kThreads) {
-    const int c = g % TC, rest = g / TC;
-    const int lo = rest & ((1 << p) - 1);
-    const int base = lo | ((rest >> p) << P);
-    double2 v[R];
+  constexpr int GPT = (G + kThreads - 1) / kThreads;
+  constexpr int CH0 = 16 / R < 1 ? 1 : 16 / R;
+  constexpr int CH = CH0 < GPT ? CH0 : GPT;
+#pragma unroll 1
+  for (int u0 = 0; u0 < GPT; u0 += CH) {
+    double2 v[CH][R];
+    int bs[CH], los[CH], cs[CH];
 #pragma unroll
-    for (int t = 0; t < R; ++t) v[t] = z[(base + (t << p)) * TC + c];
+    for (int u = 0; u < CH; ++u) {
+      const int g = threadIdx.x + (u0 + u) * kThreads;
+      const int c = g % TC, rest = g / TC;
+      los[u] = rest & ((1 << p) - 1);
+      bs[u] = los[u] | ((rest >> p) << P);
+      cs[u] = c;
+      if (g < G && u0 + u < GPT) {
 #pragma unroll
-    for (int s = 0; s < A; ++s) {
-      const int half = R >> (s + 1);
-      const int q = P - 1 - s;
-#pragma unroll
-      for (int t = 0; t < R; ++t) {
-        if (t & half) continue;
-        const double2 u = v[t], w = v[t + half];
-        v[t] = make_double2(u.x + w.x, u.y + w.y);
-        const double2 dlt = make_double2(u.x - w.x, u.y - w.y);
-        const int e = (lo | ((t & (half - 1)) << p)) << (K - 1 - q);
-        v[t + half] = e ? cmul(dlt, wN[e]) : dlt;
+        for (int t = 0; t < R; ++t) {
+          if constexpr (FIRST) v[u][t] = ld(bs[u] + (t << p), c);
+          else v[u][t] = z[(bs[u] + (t << p)) * TC + c];
+        }
       }
     }
-    if constexpr (FINAL) {
 #pragma unroll
-      for (int t = 0; t < R; ++t) epi(base + (t << p), c, v[t]);
-    } else {
+    for (int u = 0; u < CH; ++u) {
+      const int g = threadIdx.x + (u0 + u) * kThreads;
+      if (g >= G || u0 + u >= GPT) continue;
 #pragma unroll
-      for (int t = 0; t < R; ++t) z[(base + (t << p)) * TC + c] = v[t];
+      for (int s = 0; s < A; ++s) {
+        const int half = R >> (s + 1);
+        const int q = P - 1 - s;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+          if (t & half) continue;
+          const double2 a = v[u][t], w = v[u][t + half];
+          v[u][t] = make_double2(a.x + w.x, a.y + w.y);
+          const double2 dlt = make_double2(a.x - w.x, a.y - w.y);
+          const int e = (los[u] | ((t & (half - 1)) << p)) << (K - 1 - q);
+          v[u][t + half] = e ? cmul(dlt, wN[e]) : dlt;
+        }
+      }
+      if constexpr (FINAL) {
+#pragma unroll
+        for (int t = 0; t < R; ++t) epi(bs[u] + (t << p), cs[u], v[u][t]);
+      } else {
+#pragma unroll
+        for (int t = 0; t < R; ++t) z[(bs[u] + (t << p)) * TC + cs[u]] = v[u][t];
+      }
     }
   }
 }
 
-template <int K, int TC, int P, class Epi>
-__device__ __forceinline__ void dif_rounds(double2* z, const double2* wN, Epi&& epi) {
-  constexpr int A = P < 3 ? P : 3;
+// rounds of radix min(16, 2^P) from the top bits down; the first reads `ld`
+// (wN: W_N^m, m < N/2, in shared memory)
+template <int K, int TC, int P, int MAXA, class Ld, class Epi>
+__device__ __forceinline__ void dif_rounds(double2* z, const double2* wN, Ld&& ld, Epi&& epi) {
+  constexpr int A = P < MAXA ? P : MAXA;
+  constexpr bool FIRST = P == K;
   if constexpr (P - A == 0) {
-    dif_round<K, TC, P, A, true>(z, wN, epi);
+    dif_round<K, TC, P, A, FIRST, true>(z, wN, ld, epi);
   } else {
-    dif_round<K, TC, P, A, false>(z, wN, epi);
+    dif_round<K, TC, P, A, FIRST, false>(z, wN, ld, epi);
     __syncthreads();
-    dif_rounds<K, TC, P - A>(z, wN, epi);
+    dif_rounds<K, TC, P - A, MAXA>(z, wN, ld, epi);
   }
 }
 
-// complex columns per tile (pass B; pass A packs twice as many real columns)
+// complex columns per tile (pass B; pass A packs twice as many real columns):
+// 8 x 16 B = 128 B row segments.  For N = 512 the tile is 64 KB (3 CTAs/SM);
+// 4 columns (6 CTAs/SM, 64 B segments) measured slower (C3HD pass B 3.30 vs 2.93 ms)
 template <int K>
 __host__ __device__ constexpr int tile_cols() {
-  return K >= 9 ? 4 : 8;
+  return 8;
 }
 
 // W_N^m = W_n^{m n/N}, m < N/2, into shared memory
@@ -123,15 +152,17 @@ __global__ void __launch_bounds__(kThreads, 5)
                      uint64_t dkey, const double2* __restrict__ tw, double2* __restrict__ Z, int64_t ldz,
                      int64_t ctiles) {
   constexpr int N = 1 << K, TC = tile_cols<K>(), TR = 2 * TC;
-  constexpr int PER = (N * TR + kThreads - 1) / kThreads;
   extern __shared__ double2 smem[];
   double2* z = smem;
   double2* wN = smem + N * TC;
   double* sg = reinterpret_cast<double*>(wN + N / 2);
   const int64_t j1 = blockIdx.x / ctiles, c0 = (blockIdx.x % ctiles) * TR;
+  // stage the strided real tile [N][2 TC] (= the packed complex tile [N][TC]):
+  // every load in flight before the twiddles and D signs are computed
+  constexpr int PER = (N * TR + kThreads - 1) / kThreads;
   double x[PER];
 #pragma unroll
-  for (int u = 0; u < PER; ++u) {  // all loads in flight before any use
+  for (int u = 0; u < PER; ++u) {
     const int g = threadIdx.x + u * kThreads;
     const int64_t row = j1 + n1 * (g / TR), col = c0 + g % TR;
     x[u] = 0.0;
@@ -150,7 +181,8 @@ __global__ void __launch_bounds__(kThreads, 5)
     if (g < N * TR) zr[g] = sg[g / TR] * x[u];
   }
   __syncthreads();
-  dif_rounds<K, TC, K>(z, wN, [&](int i, int c, double2 v) { z[i * TC + c] = v; });
+  dif_rounds<K, TC, K, 3>(z, wN, [&](int i, int c) { return z[i * TC + c]; },
+                          [&](int i, int c, double2 v) { z[i * TC + c] = v; });
   __syncthreads();
   for (int e = threadIdx.x; e < (N / 2 + 1) * TC; e += kThreads) {
     const int k2 = e / TC, c = e % TC;
@@ -175,35 +207,24 @@ __global__ void __launch_bounds__(kThreads, 5)
                      const double2* __restrict__ tw, double* __restrict__ H, int64_t ldh, double* __restrict__ hb,
                      int64_t ctiles) {
   constexpr int N = 1 << K, TC = tile_cols<K>();
-  constexpr int PER = (N * TC + kThreads - 1) / kThreads;
   extern __shared__ double2 smem[];
   double2* z = smem;
   double2* wN = smem + N * TC;
   const int64_t n = n2 << K;
   const int64_t k2 = blockIdx.x / ctiles, c0 = (blockIdx.x % ctiles) * TC;
   const double2* src = Z + (k2 << K) * ldz + c0;
-  double2 x[PER];
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int g = threadIdx.x + u * kThreads;
-    if (g < N * TC) x[u] = src[(int64_t)(g / TC) * ldz + g % TC];
-  }
   load_wN<K>(wN, tw, n);
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int g = threadIdx.x + u * kThreads;
-    if (g < N * TC) z[g] = x[u];
-  }
   __syncthreads();
+  auto ld = [&](int j1, int c) { return src[(int64_t)j1 * ldz + c]; };
   const bool mirror = k2 > 0 && 2 * k2 < n2;
-  dif_rounds<K, TC, K>(z, wN, [&](int i, int c, double2 v) {
+  dif_rounds<K, TC, K, 4>(z, wN, ld, [&](int i, int c, double2 v) {
     const int64_t col = c0 + c;
     if (col > d || (col == d && !hb)) return;
     const int64_t k = k2 + n2 * bitrev(i, K);
     double* dst = col < d ? H + col : hb;
-    const int64_t ld = col < d ? ldh : 1;
-    dst[k * ld] = v.x - v.y;
-    if (mirror) dst[(n - k) * ld] = v.x + v.y;
+    const int64_t stride = col < d ? ldh : 1;
+    dst[k * stride] = v.x - v.y;
+    if (mirror) dst[(n - k) * stride] = v.x + v.y;
   });
 }
 
@@ -260,6 +281,10 @@ int ilog2(int64_t n) {
   return L;
 }
 
+// pass B (contiguous rows) takes the larger half of an odd L: measured faster
+// than a 9-bit strided pass A (C3HD: 6.32 vs 7.32 ms with 8-column tiles)
+int split_L1(int L) { return (L + 1) / 2; }
+
 }  // namespace
 
 bool dht_pow2_supported(int64_t n) { return n >= 4 && n <= (1ll << 18) && (n & (n - 1)) == 0; }
@@ -268,7 +293,7 @@ bool dht_pow2_supported(int64_t n) { return n >= 4 && n <= (1ll << 18) && (n & (
 int64_t dht_pow2_ldz(int64_t ncol) { return (ncol + 15) / 16 * 16; }
 
 size_t dht_pow2_z_elems(int64_t n, int64_t ncol) {
-  const int L = ilog2(n), L1 = (L + 1) / 2, L2 = L - L1;
+  const int L = ilog2(n), L1 = split_L1(L), L2 = L - L1;
   return (size_t)(((1ll << L2) / 2 + 1) << L1) * (size_t)dht_pow2_ldz(ncol);
 }
 
@@ -276,7 +301,7 @@ size_t dht_pow2_z_elems(int64_t n, int64_t ncol) {
 // Z: dht_pow2_z_elems complex; tw: n/2 + 1 complex.
 int launch_dht_pow2(int64_t n, int64_t d, const double* A, int64_t lda, const double* b, uint64_t dkey,
                     double2* Z, double2* tw, double* H, int64_t ldh, double* hb, cudaStream_t st) {
-  const int L = ilog2(n), L1 = (L + 1) / 2, L2 = L - L1;
+  const int L = ilog2(n), L1 = split_L1(L), L2 = L - L1;
   const int64_t n1 = 1ll << L1, n2 = 1ll << L2;
   const int64_t ldz = dht_pow2_ldz(d + (b ? 1 : 0));
   twiddle_kernel<<<(unsigned)((n / 2 + 1 + 255) / 256), 256, 0, st>>>(n, tw);
