@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 5)
     if (g < N * TR) zr[g] = sg[g / TR] * x[u];
   }
   __syncthreads();
-  dif_rounds<K, TC, K, 3>(z, wN, [&](int i, int c) { return z[i * TC + c]; },
+  dif_rounds<K, TC, K, 4>(z, wN, [&](int i, int c) { return z[i * TC + c]; },
                           [&](int i, int c, double2 v) { z[i * TC + c] = v; });
   __syncthreads();
   for (int e = threadIdx.x; e < (N / 2 + 1) * TC; e += kThreads) {
