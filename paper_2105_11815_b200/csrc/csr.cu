@@ -10,14 +10,14 @@
 //           nonzeros to its offset (a scan of the row lengths in bucket order).
 //           All entries are independent, so the random row reads of A are all in
 //           flight together instead of forming per-bucket dependent chains.
-//   Reduce  one CTA per bucket: its contiguous run of pairs is staged with
-//           coalesced loads; per column tile (<= 4096 fp64 columns of shared
-//           memory, zero-filled in place) the run is consumed 256 pairs at a
-//           time; pairs of one chunk that share a column are applied in rounds
-//           (integer atomicMin on a per-column claim picks the earliest pending
-//           pair, which adds its value) -- every column sees its terms in list
-//           order = ascending row, the canonical order.  The tile is streamed
-//           out once with 16-byte stores.
+//   Reduce  one CTA per bucket: its contiguous run of pairs is loaded into
+//           registers once; per column tile (<= 4096 fp64 columns of shared
+//           memory, zero-filled in place) every pair takes an arrival rank on
+//           its column; single pairs store, pairs of two add (IEEE addition
+//           commutes), longer columns are summed by one thread in list order
+//           (= ascending row, the canonical order); claim rounds are the
+//           fallback for long runs and heavy columns (csr_reduce_kernel).  The
+//           tile is streamed out once with 16-byte stores.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -30,8 +30,11 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kTileMax = 4096;   // fp64 accumulator columns per pass (32 KiB)
-constexpr int kStageCap = 2048;  // staged pairs (24 KiB)
+constexpr int kChunk = 2048;     // pairs held in registers (8 per thread)
+constexpr int kPer = 2048 / 256;
 constexpr int kFree = 0x7fffffff;
+constexpr int kSideCap = 512;    // side list (pairs of columns with >= 3) per tile
+
 
 struct CsrWs {
   int32_t* off;   // [N + 1] exclusive scan of row lengths in bucket order
@@ -96,21 +99,67 @@ __global__ void __launch_bounds__(256, 6) csr_expand_kernel(int64_t N, const int
   }
 }
 
+// Claim rounds over one chunk of pairs held in registers (pc/pv, pair e =
+// tid + k * kThreads of the chunk): each round applies, for every column, its
+// earliest pending pair (integer atomicMin on claim[]), so every column sees its
+// terms in list order.  claim[] must be kFree on entry and is kFree on exit.
+__device__ __forceinline__ void claim_rounds(double* acc, int* claim, const int (&pc)[kPer], const double (&pv)[kPer],
+                                             unsigned pend) {
+  while (__syncthreads_or(pend != 0)) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if ((pend >> k) & 1u) atomicMin(&claim[pc[k]], (int)threadIdx.x + k * kThreads);
+    __syncthreads();
+    unsigned win = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (((pend >> k) & 1u) && claim[pc[k]] == (int)threadIdx.x + k * kThreads) win |= 1u << k;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if ((win >> k) & 1u) {
+        acc[pc[k]] = acc[pc[k]] + pv[k];
+        claim[pc[k]] = kFree;
+      }
+    pend &= ~win;
+  }
+}
+
+// One CTA per bucket.  Its run of (column, signed value) pairs (list order =
+// canonical order) is loaded into registers once when it has <= kChunk pairs,
+// and per column tile (<= 4096 fp64 columns of shared memory):
+//   fast path: count each column's pairs (integer atomicAdd on word[c]); a
+//     single pair stores 0 + v; a column of two pairs takes two fp64 shared
+//     atomic adds onto 0 -- IEEE addition commutes, so (0 + a) + b == (0 + b) + a
+//     is the list-order sum whatever order they land in; the pairs of columns
+//     with more go to a side list, sorted by (column, index) by counting, and
+//     the first pair of each column's run sums the run in list order.  A few
+//     barriers per tile instead of three per round.
+//   fallback (side list over capacity, or a run longer than kChunk): claim
+//     rounds, chunk by chunk.
 __global__ void __launch_bounds__(kThreads, 3) csr_reduce_kernel(
     int64_t m, const int32_t* __restrict__ ptr, const int32_t* __restrict__ off, const int32_t* __restrict__ ecol,
     const double* __restrict__ eval, int64_t d, int tile_cols, double* __restrict__ SA, int64_t ldsa, double alpha) {
   extern __shared__ double acc[];  // [tile_cols]
-  __shared__ int s_col[kStageCap];
-  __shared__ double s_val[kStageCap];
-  __shared__ int claim[kTileMax];
+  __shared__ int word[kTileMax];
+  __shared__ int side_ci[kSideCap];  // column
+  __shared__ int side_ix[kSideCap];
+  __shared__ double side_v[kSideCap];
+  __shared__ double sorted_v[kSideCap];
+  __shared__ int sorted_c[kSideCap];
+  __shared__ int side_n, fallback;
   const int64_t b = blockIdx.x;
   const int e_beg = off[ptr[b]], e_end = off[ptr[b + 1]];
   const int ntiles = (int)((d + tile_cols - 1) / tile_cols);
-  const bool whole = e_end - e_beg <= kStageCap;
+  const bool whole = e_end - e_beg <= kChunk;
+  int pcol[kPer];
+  double pval[kPer];
   if (whole) {
-    for (int e = e_beg + (int)threadIdx.x; e < e_end; e += kThreads) {
-      s_col[e - e_beg] = ecol[e];
-      s_val[e - e_beg] = eval[e];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int e = e_beg + (int)threadIdx.x + k * kThreads;
+      pcol[k] = e < e_end ? ecol[e] : -1;
+      pval[k] = e < e_end ? eval[e] : 0.0;
     }
   }
   for (int t = 0; t < ntiles; ++t) {
@@ -119,56 +168,107 @@ __global__ void __launch_bounds__(kThreads, 3) csr_reduce_kernel(
     const int width = (int)min((int64_t)tile_cols, d - c0);
     for (int i = threadIdx.x; i < width; i += kThreads) {
       acc[i] = 0.0;
-      claim[i] = kFree;
+      word[i] = 0;
     }
-    for (int s0 = e_beg; s0 < e_end; s0 += kStageCap) {
-      const int cnt = min(kStageCap, e_end - s0);
-      if (!whole) {
-        __syncthreads();
-        for (int e = (int)threadIdx.x; e < cnt; e += kThreads) {
-          s_col[e] = ecol[s0 + e];
-          s_val[e] = eval[s0 + e];
+    if (threadIdx.x == 0) {
+      side_n = 0;
+      fallback = !whole;
+    }
+    __syncthreads();
+    if (whole) {
+      // 1. multiplicity of every column of the tile
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int cc = pcol[k] - c0i;
+        if (pcol[k] >= 0 && (unsigned)cc < (unsigned)width) atomicAdd(&word[cc], 1);
+      }
+      __syncthreads();
+      // 2. one pair: store 0 + v; two pairs: two fp64 adds onto 0 in either order
+      //    give (0 + a) + b == (0 + b) + a; more: to the side list
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int cc = pcol[k] - c0i;
+        if (pcol[k] < 0 || (unsigned)cc >= (unsigned)width) continue;
+        const int cnt = word[cc];
+        if (cnt == 1) {
+          acc[cc] = 0.0 + pval[k];
+        } else if (cnt == 2) {
+          atomicAdd(&acc[cc], pval[k]);
+        } else {
+          const int slot = atomicAdd(&side_n, 1);
+          if (slot < kSideCap) {
+            side_ci[slot] = cc;
+            side_ix[slot] = (int)threadIdx.x + k * kThreads;
+            side_v[slot] = pval[k];
+          } else {
+            fallback = 1;
+          }
         }
       }
       __syncthreads();
-      // every thread holds up to kPer pairs (e = tid + k*256); a round applies,
-      // for each column, its earliest pending pair of the whole staged run, so
-      // the number of rounds is the largest column multiplicity (a few)
-      constexpr int kPer = kStageCap / kThreads;
-      int pcol[kPer];
-      unsigned pend = 0;
+      // 3. columns of >= 3 pairs: sort the side list by (column, index) (each
+      //    entry's position = the number of entries before it), then the first
+      //    entry of each column sums its run in list order
+      const int ns = min(side_n, kSideCap);
+      if (ns > 0 && !fallback) {
+        double vi[kSideCap / kThreads];
+        int pi[kSideCap / kThreads];
 #pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const int e = (int)threadIdx.x + k * kThreads;
-        pcol[k] = 0;
-        if (e < cnt) {
-          const int cc = s_col[e] - c0i;
-          if ((unsigned)cc < (unsigned)width) {
-            pcol[k] = cc;
-            pend |= 1u << k;
-          }
+        for (int u = 0; u < kSideCap / kThreads; ++u) {
+          const int i = (int)threadIdx.x + u * kThreads;
+          pi[u] = -1;
+          if (i >= ns) continue;
+          const long long key = ((long long)side_ci[i] << 32) | (unsigned)side_ix[i];
+          int pos = 0;
+          for (int j = 0; j < ns; ++j) pos += (((long long)side_ci[j] << 32) | (unsigned)side_ix[j]) < key;
+          pi[u] = pos;
+          vi[u] = side_v[i];
         }
-      }
-      while (__syncthreads_or(pend != 0)) {
-#pragma unroll
-        for (int k = 0; k < kPer; ++k)
-          if ((pend >> k) & 1u) atomicMin(&claim[pcol[k]], (int)threadIdx.x + k * kThreads);
-        __syncthreads();
-        unsigned win = 0;
-#pragma unroll
-        for (int k = 0; k < kPer; ++k)
-          if (((pend >> k) & 1u) && claim[pcol[k]] == (int)threadIdx.x + k * kThreads) win |= 1u << k;
         __syncthreads();
 #pragma unroll
-        for (int k = 0; k < kPer; ++k)
-          if ((win >> k) & 1u) {  // the earliest pending pair of this column
-            acc[pcol[k]] = acc[pcol[k]] + s_val[threadIdx.x + k * kThreads];
-            claim[pcol[k]] = kFree;
+        for (int u = 0; u < kSideCap / kThreads; ++u)
+          if (pi[u] >= 0) {
+            sorted_v[pi[u]] = vi[u];
+            sorted_c[pi[u]] = side_ci[(int)threadIdx.x + u * kThreads];
           }
-        pend &= ~win;
+        __syncthreads();
+        for (int p0 = threadIdx.x; p0 < ns; p0 += kThreads) {
+          const int cc = sorted_c[p0];
+          if (p0 > 0 && sorted_c[p0 - 1] == cc) continue;
+          double sum = 0.0;
+          for (int p = p0; p < ns && sorted_c[p] == cc; ++p) sum = sum + sorted_v[p];
+          acc[cc] = sum;
+        }
+        __syncthreads();
       }
     }
-    __syncthreads();
+    if (fallback) {  // uniform: read after a barrier
+      for (int i = threadIdx.x; i < width; i += kThreads) {
+        acc[i] = 0.0;
+        word[i] = kFree;
+      }
+      for (int s0 = e_beg; s0 < e_end; s0 += kChunk) {
+        int pc[kPer];
+        double pv[kPer];
+        unsigned pend = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+          const int e = s0 + (int)threadIdx.x + k * kThreads;
+          pc[k] = 0;
+          pv[k] = 0.0;
+          if (e < e_end && e < s0 + kChunk) {
+            const int cc = ecol[e] - c0i;
+            if ((unsigned)cc < (unsigned)width) {
+              pc[k] = cc;
+              pv[k] = eval[e];
+              pend |= 1u << k;
+            }
+          }
+        }
+        claim_rounds(acc, word, pc, pv, pend);  // starts with a barrier
+      }
+      __syncthreads();
+    }
     double* o = SA + b * ldsa + c0;
     const bool vec = ((reinterpret_cast<uintptr_t>(o) & 15) == 0) && (width % 2 == 0);
     if (vec) {

@@ -90,3 +90,46 @@ def test_hrdht_single_row_and_prime_n():
         SA, _ = skh().hrdht_dense(1, torch.from_numpy(A).cuda(), None, m, 1)
         SAo, _ = hartley.hrdht_sketch(1, A, None, m, 1)
         assert rel(np_(SA), SAo) <= TOL
+
+
+def _csr_from_rows(cols_per_row, r):
+    n = len(cols_per_row)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum([len(c) for c in cols_per_row], out=rp[1:])
+    ci = np.concatenate([np.sort(np.asarray(c, dtype=np.int32)) for c in cols_per_row]).astype(np.int32)
+    return rp, ci, r.standard_normal(rp[-1])
+
+
+@pytest.mark.parametrize("case", ["leader", "heavy", "side_overflow", "two_tiles", "neg_zero"])
+def test_csr_reduce_paths(case):
+    """csr_reduce_kernel's paths, bit-exact against the oracle: columns of 3..24
+    pairs (one thread sums them in list order), a column in every row (over the
+    multiplicity cap: claim-round fallback), a side list over capacity, d over one
+    4096-column tile, and -0.0 values (0 + v, not v, is stored)."""
+    from oracle import sketch
+    r = np.random.default_rng(hash(case) & 0xffff)
+    if case == "leader":
+        n, d, m, s = 2400, 100, 4, 1
+        rows = [r.choice(d, size=1, replace=False) for _ in range(n)]
+    elif case == "heavy":
+        n, d, m, s = 2000, 300, 4, 1
+        rows = [np.unique(np.r_[0, r.choice(d, size=1)]) for _ in range(n)]
+    elif case == "side_overflow":
+        n, d, m, s = 1800, 40, 1, 1
+        rows = [r.choice(d, size=1) for _ in range(n)]
+    elif case == "two_tiles":
+        n, d, m, s = 3000, 9000, 3, 2
+        rows = [np.unique(np.r_[r.choice(d, size=3), r.choice(8, size=1), 4096 + r.choice(8, size=1)]) for _ in range(n)]
+    else:
+        n, d, m, s = 1000, 64, 8, 3
+        rows = [r.choice(d, size=4, replace=False) for _ in range(n)]
+    rp, ci, v = _csr_from_rows(rows, r)
+    if case == "neg_zero":
+        v[::3] = -0.0
+        v[1::3] = 0.0
+    b = r.standard_normal(n)
+    bl = skh().hash_gen(17, m, s, n)
+    SA, Sb = skh().sketch_csr(bl, torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(),
+                              torch.from_numpy(v).cuda(), d, torch.from_numpy(b).cuda())
+    SAo, Sbo = sketch.sketch_csr(17, rp, ci, v, d, b, m, s)
+    assert bits(np_(SA), SAo) and bits(np_(Sb), Sbo)
