@@ -97,25 +97,38 @@ __global__ void __launch_bounds__(kWarps * 32) gather_dense_kernel(
   }
 }
 
-// Sb: one warp per bucket.  32 entries are loaded at once (one per lane), then
-// added to the running sum in list order by lane 0 via shuffles -- the same
-// sequential order as the oracle.
+// Sb: one warp per bucket.  Up to 4 x 32 entries are loaded at once (one per
+// lane per chunk, all loads in flight together), then added to the running sum
+// in list order via shuffles -- the same sequential order as the oracle.
 __global__ void gather_vec_kernel(int64_t m, const int32_t* __restrict__ ptr, const int32_t* __restrict__ rows,
                                   const int8_t* __restrict__ sg, const double* __restrict__ x,
                                   double* __restrict__ out, double alpha) {
+  constexpr int kU = 4;
   const int lane = threadIdx.x & 31;
   const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (b >= m) return;
   const int beg = ptr[b], end = ptr[b + 1];
   double acc = 0.0;
-  for (int t0 = beg; t0 < end; t0 += 32) {
-    const int cnt = min(32, end - t0);
-    double v = 0.0;
-    if (lane < cnt) {
-      v = __ldg(x + rows[t0 + lane]);
-      if (sg[t0 + lane] < 0) v = -v;
+  for (int t0 = beg; t0 < end; t0 += 32 * kU) {
+    int r[kU];
+    int8_t g[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int t = t0 + 32 * u + lane;
+      r[u] = t < end ? rows[t] : -1;
+      g[u] = t < end ? sg[t] : 1;
     }
-    for (int u = 0; u < cnt; ++u) acc = acc + __shfl_sync(0xffffffffu, v, u);
+    double v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      v[u] = r[u] >= 0 ? __ldg(x + r[u]) : 0.0;
+      if (g[u] < 0) v[u] = -v[u];
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int cnt = min(32, end - (t0 + 32 * u));
+      for (int k = 0; k < cnt; ++k) acc = acc + __shfl_sync(0xffffffffu, v[u], k);
+    }
   }
   if (lane == 0) out[b] = alpha * acc;
 }
