@@ -234,10 +234,18 @@ __global__ void __launch_bounds__(kSortThreads) downsweep_kernel(const uint64_t*
   for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortThreads) (&wcnt[0][0])[i] = 0;
   __syncthreads();
   const int64_t wbase = (int64_t)blockIdx.x * kTile + (int64_t)w * kItemsPerWarp;
-  for (int r = 0; r < kItemsPerWarp; r += 32) {
-    int64_t e = wbase + r + lane;
-    if (e < N) atomicAdd(&wcnt[w][digit_of(in[e], shift)], 1);
+  // the warp's 512 keys in registers (16 per lane, all loads in flight at once):
+  // the ranking loop below is sequential over chunks and must not wait on memory
+  constexpr int kR = kItemsPerWarp / 32;
+  uint64_t kv[kR];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int64_t e = wbase + r * 32 + lane;
+    kv[r] = e < N ? in[e] : 0;
   }
+#pragma unroll
+  for (int r = 0; r < kR; ++r)
+    if (wbase + r * 32 + lane < N) atomicAdd(&wcnt[w][digit_of(kv[r], shift)], 1);
   __syncthreads();
   {
     const int dg = threadIdx.x;  // 256 threads = 256 digits
@@ -250,16 +258,16 @@ __global__ void __launch_bounds__(kSortThreads) downsweep_kernel(const uint64_t*
   }
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
-  for (int r = 0; r < kItemsPerWarp; r += 32) {
-    const int64_t e = wbase + r + lane;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int64_t e = wbase + r * 32 + lane;
     const bool valid = e < N;
     const unsigned vmask = __ballot_sync(0xffffffffu, valid);
     if (vmask == 0) break;
-    uint64_t key = 0;
+    const uint64_t key = kv[r];
     int dg = 0, rank = 0, base = 0;
     unsigned peers = 0;
     if (valid) {
-      key = in[e];
       dg = digit_of(key, shift);
       peers = __match_any_sync(vmask, dg);
       rank = __popc(peers & lt);
