@@ -52,7 +52,8 @@ __device__ __forceinline__ int bitrev(int i, int K) { return (int)(__brev((unsig
 
 // One register round of the DIF FFT over index bits [P - a, P) of an N = 2^K
 // point transform, TC columns, z[i * TC + c].  FIRST: the inputs come from
-// `ld(i, c)` (global memory) instead of shared memory; FINAL: P - a == 0, the
+// `ld(u, t, i, c)` (group u of the thread, point t; registers or global memory)
+// instead of shared memory; FINAL: P - a == 0, the
 // outputs go to `epi(i, c, v)` instead of back to shared memory.  A thread takes
 // CH groups at a time (all their loads issued before any butterfly), CH * 2^a
 // <= 16 complex values in registers.
@@ -64,7 +65,7 @@ __device__ __forceinline__ void dif_round(double2* __restrict__ z, const double2
   constexpr int GPT = (G + kThreads - 1) / kThreads;
   constexpr int CH0 = 16 / R < 1 ? 1 : 16 / R;
   constexpr int CH = CH0 < GPT ? CH0 : GPT;
-#pragma unroll 1
+#pragma unroll
   for (int u0 = 0; u0 < GPT; u0 += CH) {
     double2 v[CH][R];
     int bs[CH], los[CH], cs[CH];
@@ -78,7 +79,7 @@ __device__ __forceinline__ void dif_round(double2* __restrict__ z, const double2
       if (g < G && u0 + u < GPT) {
 #pragma unroll
         for (int t = 0; t < R; ++t) {
-          if constexpr (FIRST) v[u][t] = ld(bs[u] + (t << p), c);
+          if constexpr (FIRST) v[u][t] = ld(u0 + u, t, bs[u] + (t << p), c);
           else v[u][t] = z[(bs[u] + (t << p)) * TC + c];
         }
       }
@@ -114,16 +115,17 @@ __device__ __forceinline__ void dif_round(double2* __restrict__ z, const double2
 
 // rounds of radix min(16, 2^P) from the top bits down; the first reads `ld`
 // (wN: W_N^m, m < N/2, in shared memory)
-template <int K, int TC, int P, int MAXA, class Ld, class Epi>
+// (FA: radix exponent of the first round, MAXA: of the others)
+template <int K, int TC, int P, int MAXA, int FA, class Ld, class Epi>
 __device__ __forceinline__ void dif_rounds(double2* z, const double2* wN, Ld&& ld, Epi&& epi) {
-  constexpr int A = P < MAXA ? P : MAXA;
   constexpr bool FIRST = P == K;
+  constexpr int A = P < (FIRST ? FA : MAXA) ? P : (FIRST ? FA : MAXA);
   if constexpr (P - A == 0) {
     dif_round<K, TC, P, A, FIRST, true>(z, wN, ld, epi);
   } else {
     dif_round<K, TC, P, A, FIRST, false>(z, wN, ld, epi);
     __syncthreads();
-    dif_rounds<K, TC, P - A, MAXA>(z, wN, ld, epi);
+    dif_rounds<K, TC, P - A, MAXA, FA>(z, wN, ld, epi);
   }
 }
 
@@ -157,32 +159,46 @@ __global__ void __launch_bounds__(kThreads, 5)
   double2* wN = smem + N * TC;
   double* sg = reinterpret_cast<double*>(wN + N / 2);
   const int64_t j1 = blockIdx.x / ctiles, c0 = (blockIdx.x % ctiles) * TR;
-  // stage the strided real tile [N][2 TC] (= the packed complex tile [N][TC]):
-  // every load in flight before the twiddles and D signs are computed
-  constexpr int PER = (N * TR + kThreads - 1) / kThreads;
-  double x[PER];
+  // load the strided real tile straight into the first round's registers: group
+  // u of this thread, point t = packed complex column c (real columns c0 + 2c,
+  // c0 + 2c + 1) of row j1 + n1 (base + t 2^p1); every load in flight before
+  // the twiddles and D signs are computed
+  constexpr int A1 = K < 4 ? K : 4, R1 = 1 << A1, p1 = K - A1;
+  constexpr int G1 = (N >> A1) * TC, GPT1 = (G1 + kThreads - 1) / kThreads;
+  const bool pairs = ((reinterpret_cast<uintptr_t>(A) | (uintptr_t)(lda * 8)) & 15) == 0;
+  double2 pre[GPT1][R1];
 #pragma unroll
-  for (int u = 0; u < PER; ++u) {
+  for (int u = 0; u < GPT1; ++u) {
     const int g = threadIdx.x + u * kThreads;
-    const int64_t row = j1 + n1 * (g / TR), col = c0 + g % TR;
-    x[u] = 0.0;
-    if (g < N * TR) {
-      if (col < d) x[u] = A[row * lda + col];
-      else if (col == d && b) x[u] = b[row];
+    const int c = g % TC, rest = g / TC;
+    const int base = (rest & ((1 << p1) - 1)) | ((rest >> p1) << K);
+    const int64_t col = c0 + 2 * c;
+#pragma unroll
+    for (int t = 0; t < R1; ++t) {
+      const int64_t row = j1 + n1 * (base + (t << p1));
+      const double* a = A + row * lda;
+      double2 x = make_double2(0.0, 0.0);
+      if (g < G1) {
+        if (pairs && col + 1 < d) {
+          x = __ldg(reinterpret_cast<const double2*>(a + col));
+        } else {
+          x.x = col < d ? a[col] : (col == d && b) ? b[row] : 0.0;
+          x.y = col + 1 < d ? a[col + 1] : (col + 1 == d && b) ? b[row] : 0.0;
+        }
+      }
+      pre[u][t] = x;
     }
   }
   load_wN<K>(wN, tw, n1 << K);
   for (int j2 = threadIdx.x; j2 < N; j2 += kThreads) sg[j2] = dsign_row(dkey, j1 + n1 * j2);
   __syncthreads();
-  double* zr = reinterpret_cast<double*>(z);
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int g = threadIdx.x + u * kThreads;
-    if (g < N * TR) zr[g] = sg[g / TR] * x[u];
-  }
-  __syncthreads();
-  dif_rounds<K, TC, K, 4>(z, wN, [&](int i, int c) { return z[i * TC + c]; },
-                          [&](int i, int c, double2 v) { z[i * TC + c] = v; });
+  dif_rounds<K, TC, K, 4, 4>(
+      z, wN,
+      [&](int u, int t, int i, int) {
+        const double sgn = sg[i];
+        return make_double2(sgn * pre[u][t].x, sgn * pre[u][t].y);
+      },
+      [&](int i, int c, double2 v) { z[i * TC + c] = v; });
   __syncthreads();
   for (int e = threadIdx.x; e < (N / 2 + 1) * TC; e += kThreads) {
     const int k2 = e / TC, c = e % TC;
@@ -202,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 5)
 
 // pass B: K = log2 n1
 template <int K>
-__global__ void __launch_bounds__(kThreads, 5)
+__global__ void __launch_bounds__(kThreads, K >= 9 ? 3 : 5)
     dht_passB_kernel(int64_t n2, int64_t d, const double2* __restrict__ Z, int64_t ldz,
                      const double2* __restrict__ tw, double* __restrict__ H, int64_t ldh, double* __restrict__ hb,
                      int64_t ctiles) {
@@ -215,9 +231,9 @@ __global__ void __launch_bounds__(kThreads, 5)
   const double2* src = Z + (k2 << K) * ldz + c0;
   load_wN<K>(wN, tw, n);
   __syncthreads();
-  auto ld = [&](int j1, int c) { return src[(int64_t)j1 * ldz + c]; };
+  auto ld = [&](int, int, int j1, int c) { return src[(int64_t)j1 * ldz + c]; };
   const bool mirror = k2 > 0 && 2 * k2 < n2;
-  dif_rounds<K, TC, K, 4>(z, wN, ld, [&](int i, int c, double2 v) {
+  dif_rounds<K, TC, K, 4, (K >= 9 ? 5 : 4)>(z, wN, ld, [&](int i, int c, double2 v) {
     const int64_t col = c0 + c;
     if (col > d || (col == d && !hb)) return;
     const int64_t k = k2 + n2 * bitrev(i, K);
