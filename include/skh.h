@@ -354,7 +354,13 @@ int skh_srdht_dense(uint64_t seed, int64_t n, int64_t m, int64_t d,
  * creates the per-thread cuSOLVER/cuBLAS handles, so it needs the device).
  * Errors: argument errors as usual (nothing enqueued); a rank-deficient SA
  * (some r_qq == 0) is detected after Step 2 and returns SKH_EINVAL with the
- * workspace already written and x untouched. */
+ * workspace already written and x untouched.
+ * Environment (read once per process, workspace query and solve alike):
+ * SKH_LLS_HOSTLOOP=1 drives Step 4 from the host (bit-identical to the graph);
+ * SKH_LLS_RINV=1 forms M = R^{-1} once (dtrsm against I, 2 d^2 doubles more
+ * workspace) and applies it as GEMVs instead of the paper's back-solves (L1081):
+ * the same minimiser (x = M y for the LSQR solution y of min ||A M y - b||),
+ * a different rounding path. */
 size_t skh_lls_workspace_bytes(int64_t n, int64_t d, int64_t m);
 int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const double* b,
                   int64_t m, const double* SA, int64_t ldsa, const double* Sb,

@@ -287,6 +287,12 @@ enum : int {
   kItMax = 16, kNumScal = 24
 };
 
+// The scalar recurrence in the host loop's exact IEEE operations: explicit
+// round-to-nearest intrinsics, so nvcc cannot contract a*b + c into an FMA
+// (the host code has none), and the graph and the host loop stay bit-identical.
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+
 // beta = ||u||; u /= beta (when > 0); anorm2 += alpha^2 + beta^2 -- the host loop's order
 __global__ void lsqr_beta_kernel(double* sc) {
   const double beta = sqrt(sc[kSqBeta]);
@@ -294,7 +300,7 @@ __global__ void lsqr_beta_kernel(double* sc) {
   sc[kBeta] = beta;
   sc[kInvBeta] = beta > 0.0 ? 1.0 / beta : 1.0;
   sc[kNegBeta] = -beta;
-  sc[kAnorm2] = sc[kAnorm2] + alpha * alpha + beta * beta;
+  sc[kAnorm2] = add(add(sc[kAnorm2], mul(alpha, alpha)), mul(beta, beta));
 }
 
 // alpha = ||v||; the plane rotation; the (7.1) estimate; the loop condition
@@ -305,16 +311,16 @@ __global__ void lsqr_alpha_kernel(double* sc, cudaGraphConditionalHandle cond) {
   sc[kInvAlpha] = alpha > 0.0 ? 1.0 / alpha : 1.0;
   sc[kNegAlpha] = -alpha;
   const double rhobar = sc[kRhobar], phibar = sc[kPhibar];
-  const double rho = sqrt(rhobar * rhobar + beta * beta);
+  const double rho = sqrt(add(mul(rhobar, rhobar), mul(beta, beta)));
   const double c = rhobar / rho, s = beta / rho;
-  const double theta = s * alpha;
-  sc[kRhobar] = -c * alpha;
-  const double phi = c * phibar;
-  const double nphibar = s * phibar;
+  const double theta = mul(s, alpha);
+  sc[kRhobar] = mul(-c, alpha);
+  const double phi = mul(c, phibar);
+  const double nphibar = mul(s, phibar);
   sc[kPhibar] = nphibar;
   sc[kP] = phi / rho;
   sc[kQ] = -theta / rho;
-  const double arnorm = alpha * fabs(s * phi);
+  const double arnorm = mul(alpha, fabs(mul(s, phi)));
   const double it = sc[kIters] + 1.0;
   sc[kIters] = it;
   bool done;
@@ -322,7 +328,7 @@ __global__ void lsqr_alpha_kernel(double* sc, cudaGraphConditionalHandle cond) {
     sc[kTest2] = 0.0;
     done = true;
   } else {
-    const double t2 = arnorm / (sqrt(sc[kAnorm2]) * nphibar);
+    const double t2 = arnorm / mul(sqrt(sc[kAnorm2]), nphibar);
     sc[kTest2] = t2;
     done = t2 <= sc[kTau];
   }
@@ -392,6 +398,9 @@ struct LlsWs {
   int* devinfo;
   double* lwork;   // cuSOLVER workspace
   int lwork_n;
+  double* Ri;      // SKH_LLS_RINV=1: M = R^{-1} column-major [d x d] (= M^T row-major)
+  double* Rr;      // M row-major
+  double* tmp;     // [d]
   int64_t nblk, nrb;
   size_t total;
 };
@@ -400,6 +409,19 @@ int64_t gemv_t_blocks(int64_t n, int64_t d) {
   const int64_t ntc = (d + kTCols - 1) / kTCols;
   const int64_t want = std::max<int64_t>(1, (148 * 8) / ntc);
   return std::min<int64_t>(want, std::max<int64_t>(1, (n + 255) / 256));
+}
+
+// SKH_LLS_RINV=1 (opt-in): form R^{-1} once (cuBLAS dtrsm against I) and apply it
+// with dense GEMVs instead of two back-solves per LSQR iteration.  LSQR then
+// runs on A M with M = fl(R^{-1}) and returns x = M y: the same minimiser
+// whatever M's rounding (M is invertible), a different rounding path from the
+// paper's back-solve (L1081), which stays the default.
+bool rinv_mode() {
+  static const bool v = [] {
+    const char* e = getenv("SKH_LLS_RINV");
+    return e && e[0] == '1';
+  }();
+  return v;
 }
 
 LlsWs lls_layout(void* base, int64_t n, int64_t d, int64_t m, int lwork_n) {
@@ -414,7 +436,7 @@ LlsWs lls_layout(void* base, int64_t n, int64_t d, int64_t m, int lwork_n) {
   w.nblk = gemv_t_blocks(n, d);
   const int64_t nblk_cm = (n + kCmRows - 1) / kCmRows;  // column-major A^T u row blocks
   w.nrb = (n + 255) / 256;  // gemv_n CTAs (rows_per_cta = 256)
-  const int64_t nsq = std::max<int64_t>(w.nrb, (n + 4095) / 4096 + 1) + 1;
+  const int64_t nsq = std::max<int64_t>(std::max<int64_t>(w.nrb, (n + 4095) / 4096 + 1), d / 8 + 1) + 1;
   w.F = (double*)take(sizeof(double) * (size_t)m * d);
   w.tau = (double*)take(sizeof(double) * (size_t)d);
   w.qtb = (double*)take(sizeof(double) * (size_t)m);
@@ -430,6 +452,11 @@ LlsWs lls_layout(void* base, int64_t n, int64_t d, int64_t m, int lwork_n) {
   w.devinfo = (int*)take(sizeof(int) * 4);
   w.lwork = (double*)take(sizeof(double) * (size_t)std::max(lwork_n, 1));
   w.lwork_n = lwork_n;
+  if (rinv_mode()) {
+    w.Ri = (double*)take(sizeof(double) * (size_t)d * d);
+    w.Rr = (double*)take(sizeof(double) * (size_t)d * d);
+    w.tmp = (double*)take(sizeof(double) * (size_t)d);
+  }
   w.total = off;
   return w;
 }
@@ -451,8 +478,8 @@ int query_lwork(int64_t m, int64_t d, int* lw) {
 
 // out = A t + beta yin (row-major A); returns ||out||^2 through w.scal[slot] (device)
 int gemv_n(int64_t n, int64_t d, const double* A, int64_t lda, const double* t, double beta, const double* yin,
-           double* out, const LlsWs& w, int slot, cudaStream_t st, const double* bdev = nullptr) {
-  const int64_t rows = 256;
+           double* out, const LlsWs& w, int slot, cudaStream_t st, const double* bdev = nullptr,
+           int64_t rows = 256) {
   const int64_t grid = (n + rows - 1) / rows;
   if (d <= kMaxSmemX) {
     const size_t smem = sizeof(double) * (size_t)d;
@@ -531,7 +558,37 @@ int read_scal(const LlsWs& w, int slot, double* out, cudaStream_t st) {
   return SKH_OK;
 }
 
+__global__ void identity_kernel(int64_t d, double* __restrict__ X) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < d * d) X[e] = (e / d == e % d) ? 1.0 : 0.0;
+}
+
+// M = R^{-1}: cuBLAS dtrsm of R X = I, then the row-major copy Rr
+int form_rinv(Handles* h, int64_t d, const LlsWs& w, int64_t m, cudaStream_t st) {
+  identity_kernel<<<(unsigned)((d * d + 255) / 256), 256, 0, st>>>(d, w.Ri);
+  note_launch();
+  const double one = 1.0;
+  if (cublasDtrsm(h->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)d,
+                  (int)d, &one, w.F, (int)m, w.Ri, (int)d) != CUBLAS_STATUS_SUCCESS) {
+    set_error("lls: cublasDtrsm (R^{-1}) failed");
+    return SKH_ECUDA;
+  }
+  dim3 grid((unsigned)((d + 31) / 32), (unsigned)((d + 31) / 32));
+  to_colmajor_kernel<<<grid, dim3(32, 8), 0, st>>>(d, d, w.Ri, d, w.Rr);  // Rr = transpose of Ri's storage
+  note_launch();
+  return check_launch("lls: R^{-1}");
+}
+
 int trsv(Handles* h, int64_t d, const LlsWs& w, int64_t m, bool trans, double* x) {
+  if (w.Ri) {  // x = M x or M^T x, M = R^{-1}: one warp per row of a row-major matrix (rinv_mode)
+    cudaStream_t st = nullptr;
+    cublasGetStream(h->blas, &st);
+    int rc = gemv_n(d, d, trans ? w.Ri : w.Rr, d, x, 0.0, nullptr, w.tmp, w, kNumScal - 1, st, nullptr, 8);
+    if (rc) return rc;
+    if (cudaMemcpyAsync(x, w.tmp, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return check_launch("lls: R^{-1} copy");
+    return SKH_OK;
+  }
   if (cublasDtrsv(h->blas, CUBLAS_FILL_MODE_UPPER, trans ? CUBLAS_OP_T : CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)d,
                   w.F, (int)m, x, 1) != CUBLAS_STATUS_SUCCESS) {
     set_error("lls: cublasDtrsv failed");
@@ -705,6 +762,7 @@ static int lls_solve_impl(bool cm, int64_t n, int64_t d, const double* A, int64_
       }
     }
   }
+  if (w.Ri && (rc = form_rinv(h, d, w, m, st))) return rc;
   skh_trace_mark(st, "qr");
   // ---- Step 3: x_s = R^{-1} Q^T Sb
   cudaMemcpyAsync(w.qtb, Sb, sizeof(double) * (size_t)m, cudaMemcpyDeviceToDevice, st);

@@ -202,7 +202,8 @@ def test_ski_lls_dense_composite(transform):
 def test_lsqr_graph_equals_host_loop(colmajor, monkeypatch):
     """Step 4 runs as one CUDA-graph WHILE loop with the scalar recurrence on the
     device; SKH_LLS_HOSTLOOP=1 selects the host-driven loop.  Same IEEE
-    operations in the same order: bit-identical x, same iteration count."""
+    operations in the same order: bit-identical x, same iteration count
+    (also with SKH_LLS_RINV=1, where R^{-1} is applied as a GEMV)."""
     from oracle import sketch
     A, b = ill_conditioned(6000, 48, 3, 1e4)
     SA, Sb = sketch.sketch_dense(4, A, b, 150, 2)
@@ -218,3 +219,37 @@ def test_lsqr_graph_equals_host_loop(colmajor, monkeypatch):
     x2, i2 = solver(*args, colmajor=colmajor)
     assert i1 == i2 and i1["iters"] > 3
     assert torch.equal(x1, x2)
+
+
+def test_rinv_mode_same_minimiser():
+    """SKH_LLS_RINV=1 (R^{-1} formed once by dtrsm, applied as GEMVs) reaches the
+    same least-squares objective as the default back-solves (a subprocess: the
+    mode is read once per process)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, numpy as np, torch
+sys.path.insert(0, "tests")
+import paper_2105_11815_b200 as skh
+from oracle import sketch
+from test_gpu_lls import ill_conditioned
+A, b = ill_conditioned(6000, 48, 3, 1e6)
+SA, Sb = sketch.sketch_dense(4, A, b, 150, 2)
+x, info = skh.lls_solve(*(torch.from_numpy(v).cuda() for v in (A, b, SA, Sb)))
+print(json.dumps({"x": x.cpu().numpy().tolist(), "info": info}))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mode in ("0", "1"):
+        env = dict(os.environ, SKH_LLS_RINV=mode)
+        p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(json.loads(p.stdout.strip().splitlines()[-1]))
+    A, b = ill_conditioned(6000, 48, 3, 1e6)
+    r = [np.linalg.norm(A @ np.array(o["x"]) - b) for o in outs]
+    best = np.linalg.norm(A @ np.linalg.lstsq(A, b, rcond=None)[0] - b)
+    assert all(o["info"]["step"] == 4 for o in outs)
+    assert abs(outs[0]["info"]["iters"] - outs[1]["info"]["iters"]) <= 2
+    assert max(r) <= best * (1 + 1e-10)

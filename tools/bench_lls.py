@@ -37,7 +37,7 @@ for _ in range(reps):
     it = max(info["iters"], 1)
     per_it = st.get("lsqr", 0.0) / it
     gbs = 2 * cfg.a_bytes / (per_it / 1e3) / 1e9
-    print(json.dumps({"workload": name, "layout": layout, "n": cfg.n, "d": cfg.d, "m": cfg.m, "step": info["step"],
+    print(json.dumps({"workload": name, "layout": layout, "rinv": os.environ.get("SKH_LLS_RINV") == "1", "n": cfg.n, "d": cfg.d, "m": cfg.m, "step": info["step"],
                       "iters": info["iters"], "test2": info["test2"], "stages_ms": {k: round(v, 3) for k, v in st.items()},
                       "ms_per_lsqr_iter": round(per_it, 4), "A_GBps_per_iter": round(gbs, 1),
                       "frac_of_hbm_peak": round(gbs / peak, 3)}), flush=True)
