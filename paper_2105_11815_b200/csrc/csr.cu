@@ -75,27 +75,56 @@ __global__ void csr_len_kernel(int64_t N, const int32_t* __restrict__ brow, cons
   rst[t] = a;
 }
 
-__global__ void __launch_bounds__(256, 6) csr_expand_kernel(int64_t N, const int8_t* __restrict__ bsg,
-                                                            const int64_t* __restrict__ rst,
-                                                            const int32_t* __restrict__ col_idx,
-                                                            const double* __restrict__ val,
-                                                            const int32_t* __restrict__ off,
-                                                            int32_t* __restrict__ ecol, double* __restrict__ eval) {
+constexpr int kExpE = 2;  // bucket-list entries per 8-lane group (all their loads in flight together)
+
+__global__ void __launch_bounds__(256) csr_expand_kernel(int64_t N, const int8_t* __restrict__ bsg,
+                                                         const int64_t* __restrict__ rst,
+                                                         const int32_t* __restrict__ col_idx,
+                                                         const double* __restrict__ val,
+                                                         const int32_t* __restrict__ off,
+                                                         int32_t* __restrict__ ecol, double* __restrict__ eval) {
   // 8 lanes per entry: each quarter-warp copies one row's run with contiguous
-  // (coalesced) loads and stores, 4 entries per warp instruction
+  // (coalesced) loads and stores; a quarter-warp takes kExpE entries spaced by
+  // the grid's group count, and issues every load of its first 8 nonzeros per
+  // entry before any store (the random row reads are latency-bound otherwise)
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t t = gt >> 3;
+  const int64_t g = gt >> 3, ngroups = ((int64_t)gridDim.x * blockDim.x) >> 3;
   const int j = (int)(gt & 7);
-  if (t >= N) return;
-  const bool neg = bsg[t] < 0;
-  const int64_t rs = rst[t];
-  const int o = off[t];
-  const int len = off[t + 1] - o;
-  for (int k = j; k < len; k += 8) {
-    const int c = col_idx[rs + k];
-    const double x = val[rs + k];
-    ecol[o + k] = c;
-    eval[o + k] = neg ? -x : x;
+  int64_t rs[kExpE];
+  int o[kExpE], len[kExpE];
+  bool neg[kExpE];
+#pragma unroll
+  for (int u = 0; u < kExpE; ++u) {
+    const int64_t t = g + u * ngroups;
+    len[u] = 0;
+    if (t < N) {
+      neg[u] = bsg[t] < 0;
+      rs[u] = rst[t];
+      o[u] = off[t];
+      len[u] = off[t + 1] - o[u];
+    }
+  }
+  int c[kExpE];
+  double x[kExpE];
+#pragma unroll
+  for (int u = 0; u < kExpE; ++u) {
+    if (j < len[u]) {
+      c[u] = col_idx[rs[u] + j];
+      x[u] = val[rs[u] + j];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kExpE; ++u) {
+    if (j < len[u]) {
+      ecol[o[u] + j] = c[u];
+      eval[o[u] + j] = neg[u] ? -x[u] : x[u];
+    }
+    for (int k = j + 8; k < len[u]; k += 8) {  // rows longer than 8 nonzeros
+      const int cc = col_idx[rs[u] + k];
+      const double xx = val[rs[u] + k];
+      ecol[o[u] + k] = cc;
+      eval[o[u] + k] = neg[u] ? -xx : xx;
+    }
   }
 }
 
@@ -305,8 +334,8 @@ int launch_gather_csr(int64_t m, int s, const int32_t* ptr, const int32_t* rows,
   rc = launch_excl_scan_i32(w.off, N + 1, w.bs, st);
   if (rc) return rc;
   if (N > 0) {
-    csr_expand_kernel<<<(unsigned)((N * 8 + 255) / 256), 256, 0, st>>>(N, sg, w.rst, col_idx, val, w.off, w.ecol,
-                                                                        w.eval);
+    csr_expand_kernel<<<(unsigned)(((N + kExpE - 1) / kExpE * 8 + 255) / 256), 256, 0, st>>>(
+        N, sg, w.rst, col_idx, val, w.off, w.ecol, w.eval);
     note_launch();
   }
   const int tile = (int)(d < kTileMax ? d : kTileMax);
