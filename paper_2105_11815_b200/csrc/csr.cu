@@ -195,10 +195,9 @@ __global__ void __launch_bounds__(kThreads, 3) csr_reduce_kernel(
     const int64_t c0 = (int64_t)t * tile_cols;
     const int c0i = (int)c0;  // d < 2^31
     const int width = (int)min((int64_t)tile_cols, d - c0);
-    for (int i = threadIdx.x; i < width; i += kThreads) {
-      acc[i] = 0.0;
-      word[i] = 0;
-    }
+    // acc is not zero-filled: the fast path zeroes the columns it touches and
+    // the write-out emits 0 where word[] is 0 (the fallback fills acc itself)
+    for (int i = threadIdx.x; i < width; i += kThreads) word[i] = 0;
     if (threadIdx.x == 0) {
       side_n = 0;
       fallback = !whole;
@@ -209,7 +208,10 @@ __global__ void __launch_bounds__(kThreads, 3) csr_reduce_kernel(
 #pragma unroll
       for (int k = 0; k < kPer; ++k) {
         const int cc = pcol[k] - c0i;
-        if (pcol[k] >= 0 && (unsigned)cc < (unsigned)width) atomicAdd(&word[cc], 1);
+        if (pcol[k] >= 0 && (unsigned)cc < (unsigned)width) {
+          atomicAdd(&word[cc], 1);
+          acc[cc] = 0.0;
+        }
       }
       __syncthreads();
       // 2. one pair: store 0 + v; two pairs: two fp64 adds onto 0 in either order
@@ -302,11 +304,12 @@ __global__ void __launch_bounds__(kThreads, 3) csr_reduce_kernel(
     const bool vec = ((reinterpret_cast<uintptr_t>(o) & 15) == 0) && (width % 2 == 0);
     if (vec) {
       for (int i = threadIdx.x; i < width / 2; i += kThreads) {
-        const double2 x = make_double2(alpha * acc[2 * i], alpha * acc[2 * i + 1]);
+        const double2 x = make_double2(word[2 * i] ? alpha * acc[2 * i] : 0.0,
+                                       word[2 * i + 1] ? alpha * acc[2 * i + 1] : 0.0);
         *reinterpret_cast<double2*>(o + 2 * i) = x;
       }
     } else {
-      for (int i = threadIdx.x; i < width; i += kThreads) o[i] = alpha * acc[i];
+      for (int i = threadIdx.x; i < width; i += kThreads) o[i] = word[i] ? alpha * acc[i] : 0.0;
     }
     __syncthreads();
   }
