@@ -1,7 +1,9 @@
 // gather.cu -- R5 for dense X: SA[b, :] = alpha * (ascending-row signed sum of
 // X rows in bucket b)  (Alg. 1 Step 1; R10).
 //
-// Work unit: one warp = one bucket x one 64-column tile; each lane owns two
+// Work unit (gather_wide_kernel, the default for even d > 64): one warp = one
+// bucket x 128 columns, each lane two pairs of adjacent columns, 4 rows in flight.
+// gather_dense_kernel (other layouts): one warp = one bucket x one 64-column tile; each lane owns two
 // adjacent columns (one 16-byte load per row) and adds the bucket's rows
 // sequentially in list order, so every output is the oracle's exact sum.  No
 // atomics, no cross-lane reduction.  Rows are prefetched kU at a time (row ids
@@ -13,6 +15,7 @@
 // L2 (C3: 131072 x 512 B = 64 MiB < 126 MB).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -97,6 +100,61 @@ __global__ void __launch_bounds__(kWarps * 32) gather_dense_kernel(
   }
 }
 
+// Wide variant: one warp = one bucket x 128 columns (two 512-byte row segments
+// per row, lane owns columns c0 + 2 lane + {0,1} and c0 + 64 + 2 lane + {0,1}),
+// 4 rows in flight per lane.  VEC2 layouts only.
+__global__ void __launch_bounds__(kWarps * 32) gather_wide_kernel(
+    int64_t m, int64_t nbgroups, const int32_t* __restrict__ ptr, const int32_t* __restrict__ rows,
+    const int8_t* __restrict__ sg, int64_t d, const double* __restrict__ X, int64_t ldx,
+    double* __restrict__ SA, int64_t ldsa, double alpha) {
+  constexpr int kW = 4;  // 2: C3 0.983 ms, 8: 1.085 ms (102 registers)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t tile = blockIdx.x / nbgroups;
+  const int64_t b = (blockIdx.x % nbgroups) * kWarps + w;
+  if (b >= m) return;
+  const int64_t ca = tile * 128 + 2 * lane, cb = ca + 64;
+  const bool va = ca < d, vb = cb < d;  // d even: pairs are whole
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+  const int beg = ptr[b], end = ptr[b + 1];
+  for (int t0 = beg; t0 < end; t0 += 32) {
+    const int cnt = min(32, end - t0);
+    int my_row = 0, my_neg = 0;
+    if (lane < cnt) {
+      my_row = rows[t0 + lane];
+      my_neg = sg[t0 + lane] < 0;
+    }
+    for (int u0 = 0; u0 < cnt; u0 += kW) {
+      double2 xa[kW], xb[kW];
+      int ng[kW];
+#pragma unroll
+      for (int u = 0; u < kW; ++u) {
+        const int src = u0 + u;
+        const int r = __shfl_sync(0xffffffffu, my_row, src & 31);
+        ng[u] = __shfl_sync(0xffffffffu, my_neg, src & 31);
+        xa[u] = make_double2(0.0, 0.0);
+        xb[u] = make_double2(0.0, 0.0);
+        if (src < cnt) {
+          const double* p = X + (int64_t)r * ldx;
+          if (va) xa[u] = __ldg(reinterpret_cast<const double2*>(p + ca));
+          if (vb) xb[u] = __ldg(reinterpret_cast<const double2*>(p + cb));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kW; ++u) {
+        if (u0 + u < cnt) {
+          a0 = ng[u] ? a0 - xa[u].x : a0 + xa[u].x;
+          a1 = ng[u] ? a1 - xa[u].y : a1 + xa[u].y;
+          b0 = ng[u] ? b0 - xb[u].x : b0 + xb[u].x;
+          b1 = ng[u] ? b1 - xb[u].y : b1 + xb[u].y;
+        }
+      }
+    }
+  }
+  double* o = SA + b * ldsa;
+  if (va) *reinterpret_cast<double2*>(o + ca) = make_double2(alpha * a0, alpha * a1);
+  if (vb) *reinterpret_cast<double2*>(o + cb) = make_double2(alpha * b0, alpha * b1);
+}
+
 // Sb: one warp per bucket.  Up to 4 x 32 entries are loaded at once (one per
 // lane per chunk, all loads in flight together), then added to the running sum
 // in list order via shuffles -- the same sequential order as the oracle.
@@ -146,6 +204,19 @@ int launch_gather_dense(int64_t m, const int32_t* ptr, const int32_t* rows, cons
   }
   const bool vec2 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(SA)) % 16 == 0) &&
                     (ldx % 2 == 0) && (ldsa % 2 == 0);
+  // 128 columns per warp (1 KB of each row) unless SKH_GATHER_WIDE=0; measured
+  // C3 gather 1.019 -> 0.956 ms, C5 10.01 -> 9.72 ms
+  static const bool wide = [] {
+    const char* e = getenv("SKH_GATHER_WIDE");
+    return !(e && e[0] == '0');
+  }();
+  if (wide && vec2 && d % 2 == 0 && d > 64) {
+    const int64_t nt = (d + 127) / 128;
+    gather_wide_kernel<<<(unsigned)(nbgroups * nt), kWarps * 32, 0, st>>>(m, nbgroups, ptr, rows, sg, d, X, ldx, SA,
+                                                                          ldsa, alpha);
+    note_launch();
+    return check_launch("gather_wide");
+  }
   if (vec2)
     gather_dense_kernel<true><<<(unsigned)grid, kWarps * 32, 0, st>>>(m, nbgroups, ptr, rows, sg, d, X, ldx, SA,
                                                                        ldsa, alpha);
