@@ -267,7 +267,7 @@ def roofline(cfg, step, stage_ms, peak_gbs, peak_src, layout="row", sketch="hash
         alg = 2 * step.n_pad * cfg.d * 8          # read + write the n x d block once per pass
         t = sum(stage_ms[k] for k in passes) / len(passes)
     else:
-        name = "gather_dense"
+        name = "gather_wide" if (cfg.d % 2 == 0 and cfg.d > 64) else "gather_dense"  # csrc/gather.cu kernel
         alg = cfg.n * cfg.d * 8 + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5
         t = stage_ms["gather"]
     achieved = alg / (t / 1e3) / 1e9
