@@ -40,17 +40,22 @@ bool dht_pow2_supported(int64_t n);
 size_t dht_pow2_z_elems(int64_t n, int64_t ncol);
 int launch_dht_pow2(int64_t n, int64_t d, const double* A, int64_t lda, const double* b, uint64_t dkey,
                     double2* Z, double2* tw, double* H, int64_t ldh, double* hb, cudaStream_t st);
+bool dht_pow2_cm_supported(int64_t n);
+size_t dht_pow2_cm_z_elems(int64_t n, int64_t ncols);
+int launch_dht_pow2_cm(int64_t n, int64_t ncolX, const double* X, int64_t ldx, const double* xb, uint64_t dkey,
+                       double2* Z, double2* tw, double* H, int64_t ldh, cudaStream_t st);
 
 namespace {
 
-// Row-major A with n = 2^L (4 <= n <= 2^18) takes the fht.cu passes unless
-// SKH_DHT_CUFFT=1 (kept for comparison: D + transpose, cuFFT D2Z, transpose).
+// n = 2^L takes the fht.cu passes (row-major 4 <= n <= 2^18, column-major
+// 256 <= n <= 2^18) unless SKH_DHT_CUFFT=1 (kept for comparison: D + layout
+// change, cuFFT D2Z, Hartley combine).
 bool use_pow2(int64_t n, bool rowmajor) {
   static const bool force_cufft = [] {
     const char* e = getenv("SKH_DHT_CUFFT");
     return e && e[0] == '1';
   }();
-  return rowmajor && !force_cufft && dht_pow2_supported(n);
+  return !force_cufft && (rowmajor ? dht_pow2_supported(n) : dht_pow2_cm_supported(n));
 }
 
 __device__ __forceinline__ double dsign(uint64_t dkey, int64_t g) {
@@ -191,8 +196,12 @@ DhtWs dht_layout(void* base, int64_t n, int64_t m, int s, int64_t d, bool rowmaj
     return q;
   };
   const int64_t ncol = d + 1;
-  if (pow2) {
+  if (pow2 && rowmajor) {
     w.Z = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * dht_pow2_z_elems(n, ncol));
+    w.tw = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * (size_t)(n / 2 + 1));
+  } else if (pow2) {
+    w.Y = (double*)take(sizeof(double) * (size_t)n * ncol);
+    w.Z = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * dht_pow2_cm_z_elems(n, ncol));
     w.tw = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * (size_t)(n / 2 + 1));
   } else {
     w.Y = (double*)take(sizeof(double) * (size_t)n * ncol);
@@ -293,9 +302,17 @@ int hrdht_run(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const d
   skh_trace_mark(st, "hash_gen");
   const uint64_t dkey = key_diag(seed);
   const double c = 1.0 / sqrt((double)n * (double)s);
-  if (pow2) {
+  if (pow2 && rowmajor) {
     if ((rc = launch_dht_pow2(n, d, A, lda, b, dkey, (double2*)w.Z, (double2*)w.tw, w.H, d, w.hb, st))) return rc;
     return finish_rowmajor(seed, n, m, d, w, b, SA, ldsa, Sb, c, sample, st);
+  }
+  if (pow2) {  // column-major, n = 2^L >= 256: H = Fhat D [A | b] into Y, then the tile gather
+    if ((rc = launch_dht_pow2_cm(n, d, A, lda, b, dkey, (double2*)w.Z, (double2*)w.tw, w.Y, n, st))) return rc;
+    if ((rc = launch_cm_gather(w.Y, n, ncol, nullptr, n, (n + 4095) / 4096, 12, 0, w.lists, s, m, SA, ldsa, d, Sb, c,
+                               st)))
+      return rc;
+    skh_trace_mark(st, "gather");
+    return SKH_OK;
   }
   if (rowmajor) {
     dim3 grid((unsigned)((d + 31) / 32), (unsigned)((n + 31) / 32));

@@ -34,8 +34,9 @@ def rel(a, b):
 
 CASES = [(1, 1, 1, 1), (2, 3, 2, 1), (7, 2, 5, 2), (100, 17, 16, 2), (1000, 64, 112, 1), (4097, 33, 200, 3),
          (65536, 8, 448, 1), (100003, 3, 1000, 2)]
-# n = 2^L, 2 <= L <= 18, row-major: the two-pass transform of csrc/fht.cu (every
-# tile size 2..512, column tiles 8/16 with ragged tails, the 2^19 cuFFT fallback)
+# n = 2^L, 2 <= L <= 18: the two-pass transforms of csrc/fht.cu (row-major: every
+# tile size 2..512, column tiles 8/16 with ragged tails; column-major from n = 256;
+# the 2^19 cuFFT fallback)
 POW2 = [(4, 1, 2, 1), (8, 15, 4, 2), (16, 16, 8, 1), (32, 17, 8, 3), (512, 33, 64, 2), (1024, 7, 100, 1),
         (4096, 40, 300, 2), (1 << 17, 9, 700, 2), (1 << 18, 5, 800, 1), (1 << 19, 2, 900, 1)]
 
@@ -51,7 +52,7 @@ def test_hrdht_rowmajor(n, d, m, s):
     assert rel(np_(SA), SAo) <= TOL and rel(np_(Sb), Sbo) <= TOL
 
 
-@pytest.mark.parametrize("n,d,m,s", CASES)
+@pytest.mark.parametrize("n,d,m,s", CASES + POW2)
 def test_hrdht_colmajor(n, d, m, s):
     from oracle import hartley
     r = np.random.default_rng(n + 2 * d)
