@@ -563,6 +563,154 @@ __global__ void cm_lists_kernel(const int32_t* __restrict__ col_rows, const int8
   }
 }
 
+// The same lists from W warps per tile (W <= 8, limited by W per-warp bucket
+// counters of m uint16 in shared memory): the tile's entries are cut into W
+// contiguous segments; (1) each warp counts its segment's buckets; (2) a
+// prefix over warps gives every warp the number of earlier same-bucket entries,
+// so it ranks its segment exactly as the one-warp walk would, adding to the
+// rank-group histogram and to per-warp key counts; (3) prefixes of those
+// counts give every warp its first slot per key, and a second ranking walk
+// places the entries.  The lists are identical to cm_lists_kernel's.
+__global__ void cm_lists_par_kernel(const int32_t* __restrict__ col_rows, const int8_t* __restrict__ col_signs,
+                                    int s, int64_t m, int K2, int lo, int64_t nvalid, int ncls,
+                                    uint32_t* __restrict__ lists, int32_t* __restrict__ roff) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int W = blockDim.x >> 5;
+  int32_t* hist = reinterpret_cast<int32_t*>(smraw);  // [512]
+  int32_t* off = hist + 512;                          // [64]: offsets + padded flag
+  int32_t* kcp = off + 64;                            // [W][512] key counts (padded keys)
+  int32_t* kcq = kcp + W * 512;                       // [W][32]  key counts (plain keys)
+  uint16_t* cntw = reinterpret_cast<uint16_t*>(kcq + W * 32);  // [W][m]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t tt = blockIdx.x;
+  const unsigned lt = (1u << lane) - 1u;
+  const int cap = list_cap(s);
+  uint32_t* out = lists + tt * (int64_t)cap;
+  const int ne = kE * s, seg = ne / W, e_lo = w * seg, e_hi = e_lo + seg;
+  uint16_t* cnt = cntw + (int64_t)w * m;
+  for (int64_t b = lane; b < m; b += 32) cnt[b] = 0;
+  for (int i = lane; i < 512; i += 32) kcp[w * 512 + i] = 0;
+  kcq[w * 32 + lane] = 0;
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) hist[i] = 0;
+  auto entry = [&](int e, int& bk, int& neg) {
+    const int p = e / s, q = e - p * s;
+    const int64_t r = tile_row(tt, p, K2, lo);
+    bk = -1;
+    neg = 0;
+    if (r < nvalid) {
+      bk = col_rows[r * s + q];
+      neg = col_signs[r * s + q] < 0;
+    }
+  };
+  __syncthreads();
+  // (1) per-warp bucket counts
+  for (int e0 = e_lo; e0 < e_hi; e0 += 32) {
+    int bk, neg;
+    entry(e0 + lane, bk, neg);
+    const unsigned grp = __match_any_sync(0xffffffffu, bk);
+    if (bk >= 0 && (grp & lt) == 0) cnt[bk] = (uint16_t)(cnt[bk] + __popc(grp));
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int64_t b = threadIdx.x; b < m; b += blockDim.x) {  // exclusive prefix over warps
+    int run = 0;
+    for (int v = 0; v < W; ++v) {
+      const int c = cntw[(int64_t)v * m + b];
+      cntw[(int64_t)v * m + b] = (uint16_t)run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  // (2) ranks -> rank-group histogram and per-warp key counts
+  for (int e0 = e_lo; e0 < e_hi; e0 += 32) {
+    int bk, neg;
+    entry(e0 + lane, bk, neg);
+    const bool valid = bk >= 0;
+    const unsigned grp = __match_any_sync(0xffffffffu, bk);
+    const int base = valid ? (int)cnt[bk] : 0;
+    __syncwarp();
+    const int rank = base + __popc(grp & lt);
+    if (valid && (grp & lt) == 0) cnt[bk] = (uint16_t)(base + __popc(grp));
+    __syncwarp();
+    if (valid) {
+      const int rk = min(rank, kRounds - 1);
+      atomicAdd(&hist[rk * 16 + (bk & (ncls - 1))], 1);
+      atomicAdd(&kcp[w * 512 + rk * 16 + (bk & (ncls - 1))], 1);
+      atomicAdd(&kcq[w * 32 + rk], 1);
+    }
+  }
+  __syncthreads();
+  for (int64_t b = threadIdx.x; b < m; b += blockDim.x) {  // counters back to the prefixes
+    for (int v = W - 1; v >= 1; --v) cntw[(int64_t)v * m + b] = cntw[(int64_t)(v - 1) * m + b];
+    cntw[b] = 0;
+  }
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < kRounds; ++i) {  // padded group lengths
+      int mx = 0;
+      for (int c = 0; c < ncls; ++c) mx = max(mx, hist[i * 16 + c]);
+      off[i] = acc;
+      acc += ncls * mx;
+    }
+    off[kRounds] = acc;
+    if (acc > cap) {  // plain order
+      acc = 0;
+      for (int i = 0; i < kRounds; ++i) {
+        int t = 0;
+        for (int c = 0; c < ncls; ++c) t += hist[i * 16 + c];
+        off[i] = acc;
+        acc += t;
+      }
+      off[kRounds] = acc;
+      off[kRounds + 1] = 0;
+    } else {
+      off[kRounds + 1] = 1;
+    }
+    for (int i = 0; i <= kRounds; ++i) roff[tt * kRoffStride + i] = off[i];
+  }
+  __syncthreads();
+  const bool padded = off[kRounds + 1] != 0;
+  // per-warp first slot index per key: exclusive prefix over warps
+  for (int key = threadIdx.x; key < 512; key += blockDim.x) {
+    int run = 0;
+    for (int v = 0; v < W; ++v) {
+      int* c = padded ? &kcp[v * 512 + key] : (key < 32 ? &kcq[v * 32 + key] : nullptr);
+      if (!c) break;
+      const int x = *c;
+      *c = run;
+      run += x;
+    }
+  }
+  if (padded)
+    for (int i = threadIdx.x; i < off[kRounds]; i += blockDim.x) out[i] = kPadWord;
+  __syncthreads();
+  // (3) rank again and place
+  int32_t* cur = padded ? kcp + w * 512 : kcq + w * 32;
+  for (int e0 = e_lo; e0 < e_hi; e0 += 32) {
+    const int e = e0 + lane;
+    int bk, neg;
+    entry(e, bk, neg);
+    const bool valid = bk >= 0;
+    const unsigned grp = __match_any_sync(0xffffffffu, bk);
+    const int base = valid ? (int)cnt[bk] : 0;
+    __syncwarp();
+    const int rank = base + __popc(grp & lt);
+    if (valid && (grp & lt) == 0) cnt[bk] = (uint16_t)(base + __popc(grp));
+    __syncwarp();
+    const int rk = min(rank, kRounds - 1);
+    const int key = padded ? rk * 16 + (bk & (ncls - 1)) : rk;
+    const unsigned g2 = __match_any_sync(0xffffffffu, valid ? key : -1);
+    const int idx = valid ? cur[key] + __popc(g2 & lt) : 0;
+    __syncwarp();
+    if (valid && (g2 & lt) == 0) cur[key] += __popc(g2);
+    __syncwarp();
+    if (valid) {
+      const int slot = padded ? off[rk] + ncls * idx + (bk & (ncls - 1)) : off[rk] + idx;
+      out[slot] = (uint32_t)(e / s) | ((uint32_t)bk << kLE) | ((uint32_t)neg << 31);
+    }
+  }
+}
+
 template <int K2, bool GATHER, int NC>
 int launch_pass2_nc(const PassArgs& a, cudaStream_t st) {
   const size_t tileb = (size_t)NC * kE * 8;
@@ -677,10 +825,26 @@ int launch_cm_lists(const int32_t* col_rows, const int8_t* col_signs, int s, int
   uint32_t* lists = static_cast<uint32_t*>(lists_ws);
   int32_t* roff = reinterpret_cast<int32_t*>(static_cast<char*>(lists_ws) +
                                              align_up(sizeof(uint32_t) * (size_t)ntiles * list_cap(s)));
+  const int ncls = 16;  // 8-byte SA entries: conflict-free half-warps
+  static const bool one_warp = [] {
+    const char* e = getenv("SKH_CM_LISTS_1W");
+    return e && e[0] == '1';
+  }();
+  // W warps per tile while W per-warp m-entry counters fit (<= 200 KB)
+  int W = 8;
+  while (W > 1 && (size_t)W * (sizeof(int32_t) * 544 + sizeof(uint16_t) * (size_t)m) + 2304 > 200 * 1024) W >>= 1;
+  if (!one_warp && W >= 2) {
+    const size_t smem = 2304 + (size_t)W * sizeof(int32_t) * 544 + align_up(sizeof(uint16_t) * (size_t)W * m, 16);
+    int rc = set_smem(cm_lists_par_kernel, smem);
+    if (rc) return rc;
+    cm_lists_par_kernel<<<(unsigned)ntiles, 32 * W, smem, st>>>(col_rows, col_signs, s, m, K2, lo, nvalid, ncls,
+                                                                 lists, roff);
+    note_launch();
+    return check_launch("cm_lists_par");
+  }
   const size_t smem = 8192 + align_up(sizeof(uint16_t) * (size_t)m, 16);
   int rc = set_smem(cm_lists_kernel, smem);
   if (rc) return rc;
-  const int ncls = 16;  // 8-byte SA entries: conflict-free half-warps
   cm_lists_kernel<<<(unsigned)ntiles, 32, smem, st>>>(col_rows, col_signs, s, m, K2, lo, nvalid, ncls, lists, roff);
   note_launch();
   return check_launch("cm_lists");
