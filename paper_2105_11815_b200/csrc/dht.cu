@@ -40,22 +40,18 @@ bool dht_pow2_supported(int64_t n);
 size_t dht_pow2_z_elems(int64_t n, int64_t ncol);
 int launch_dht_pow2(int64_t n, int64_t d, const double* A, int64_t lda, const double* b, uint64_t dkey,
                     double2* Z, double2* tw, double* H, int64_t ldh, double* hb, cudaStream_t st);
-bool dht_pow2_cm_supported(int64_t n);
-size_t dht_pow2_cm_z_elems(int64_t n, int64_t ncols);
-int launch_dht_pow2_cm(int64_t n, int64_t ncolX, const double* X, int64_t ldx, const double* xb, uint64_t dkey,
-                       double2* Z, double2* tw, double* H, int64_t ldh, cudaStream_t st);
 
 namespace {
 
-// n = 2^L takes the fht.cu passes (row-major 4 <= n <= 2^18, column-major
-// 256 <= n <= 2^18) unless SKH_DHT_CUFFT=1 (kept for comparison: D + layout
-// change, cuFFT D2Z, Hartley combine).
+// n = 2^L (4 <= n <= 2^18) takes the fht.cu passes -- column-major A through a
+// tiled transpose first -- unless SKH_DHT_CUFFT=1 (kept for comparison: D +
+// layout change, cuFFT D2Z, Hartley combine).
 bool use_pow2(int64_t n, bool rowmajor) {
   static const bool force_cufft = [] {
     const char* e = getenv("SKH_DHT_CUFFT");
     return e && e[0] == '1';
   }();
-  return !force_cufft && (rowmajor ? dht_pow2_supported(n) : dht_pow2_cm_supported(n));
+  return !force_cufft && dht_pow2_supported(n);
 }
 
 __device__ __forceinline__ double dsign(uint64_t dkey, int64_t g) {
@@ -76,6 +72,52 @@ __global__ void diag_transpose_kernel(int64_t n, int64_t d, const double* __rest
     const int64_t c = c0 + k, r = r0 + threadIdx.x;
     if (r < n && c < d) Y[c * n + r] = dsign(dkey, r) * tile[threadIdx.x][k];
   }
+}
+
+// Y[i * ldy + c] = X[c * ldx + i]: column-major n x d -> row-major, 64 x 64
+// tiles, 16-byte accesses on both sides when X, Y and the strides are even
+// (512 bytes per warp instruction), 2-way shared-memory conflicts at most.
+template <bool V2>
+__global__ void __launch_bounds__(256) cm_to_rm_kernel(int64_t n, int64_t d, const double* __restrict__ X,
+                                                       int64_t ldx, double* __restrict__ Y, int64_t ldy) {
+  __shared__ double tile[64][65];  // [c][i]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
+  for (int k = w; k < 64; k += 8) {  // column c0 + k, rows i0 + 2 lane, + 1
+    const int64_t c = c0 + k, i = i0 + 2 * lane;
+    double2 v = make_double2(0.0, 0.0);
+    if (c < d) {
+      if (V2 && i + 1 < n) {
+        v = __ldg(reinterpret_cast<const double2*>(X + c * ldx + i));
+      } else {
+        if (i < n) v.x = X[c * ldx + i];
+        if (i + 1 < n) v.y = X[c * ldx + i + 1];
+      }
+    }
+    tile[k][2 * lane] = v.x;
+    tile[k][2 * lane + 1] = v.y;
+  }
+  __syncthreads();
+  for (int k = w; k < 64; k += 8) {  // row i0 + k, columns c0 + 2 lane, + 1
+    const int64_t i = i0 + k, c = c0 + 2 * lane;
+    if (i >= n) continue;
+    const double2 v = make_double2(tile[2 * lane][k], tile[2 * lane + 1][k]);
+    if (V2 && c + 1 < d) {
+      *reinterpret_cast<double2*>(Y + i * ldy + c) = v;
+    } else {
+      if (c < d) Y[i * ldy + c] = v.x;
+      if (c + 1 < d) Y[i * ldy + c + 1] = v.y;
+    }
+  }
+}
+
+void transpose_cm_to_rm(int64_t n, int64_t d, const double* X, int64_t ldx, double* Y, int64_t ldy, cudaStream_t st) {
+  const bool v2 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) % 16 == 0) && ldx % 2 == 0 &&
+                  ldy % 2 == 0;
+  dim3 g((unsigned)((n + 63) / 64), (unsigned)((d + 63) / 64));
+  if (v2) cm_to_rm_kernel<true><<<g, 256, 0, st>>>(n, d, X, ldx, Y, ldy);
+  else cm_to_rm_kernel<false><<<g, 256, 0, st>>>(n, d, X, ldx, Y, ldy);
+  note_launch();
 }
 
 // Y[c * n + i] = D_i X[c * ldx + i] (column-major X) for c < ncol
@@ -174,6 +216,7 @@ struct DhtWs {
   cufftDoubleComplex* tw;    // fht.cu: W_n^e, e <= n/2
   double* H;                 // row-major Fhat D A [n][d] (row-major path)
   double* hb;                // Fhat D b [n] (row-major path)
+  double* SAt;               // column-major power-of-two path: row-major SA before the transpose
   void* fftwork;
   int32_t* col_rows;
   int8_t* col_signs;
@@ -196,13 +239,14 @@ DhtWs dht_layout(void* base, int64_t n, int64_t m, int s, int64_t d, bool rowmaj
     return q;
   };
   const int64_t ncol = d + 1;
-  if (pow2 && rowmajor) {
+  if (pow2) {  // column-major input is transposed into H first (row-major kernels, §5d)
     w.Z = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * dht_pow2_z_elems(n, ncol));
     w.tw = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * (size_t)(n / 2 + 1));
-  } else if (pow2) {
-    w.Y = (double*)take(sizeof(double) * (size_t)n * ncol);
-    w.Z = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * dht_pow2_cm_z_elems(n, ncol));
-    w.tw = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * (size_t)(n / 2 + 1));
+    if (!rowmajor) {
+      w.H = (double*)take(sizeof(double) * (size_t)n * d);
+      w.hb = (double*)take(sizeof(double) * (size_t)n);
+      w.SAt = (double*)take(sizeof(double) * (size_t)m * d);
+    }
   } else {
     w.Y = (double*)take(sizeof(double) * (size_t)n * ncol);
     w.Z = (cufftDoubleComplex*)take(sizeof(cufftDoubleComplex) * (size_t)(n / 2 + 1) * ncol);
@@ -218,7 +262,7 @@ DhtWs dht_layout(void* base, int64_t n, int64_t m, int s, int64_t d, bool rowmaj
   w.rows = (int32_t*)take(sizeof(int32_t) * (size_t)n * s);
   w.signs = (int8_t*)take((size_t)n * s);
   w.hws = take(hash_ws_bytes(n, m, s));
-  if (!rowmajor) w.lists = take(cm_lists_bytes((n + 4095) / 4096, s));
+  if (!rowmajor && !pow2) w.lists = take(cm_lists_bytes((n + 4095) / 4096, s));
   w.total = off;
   return w;
 }
@@ -297,7 +341,8 @@ int hrdht_run(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const d
                      hash_ws_bytes(n, m, s), st);
     if (rc) return rc;
   }
-  if (!rowmajor && (rc = launch_cm_lists(w.col_rows, w.col_signs, s, m, 0, 12, n, (n + 4095) / 4096, w.lists, st)))
+  if (!rowmajor && !pow2 &&
+      (rc = launch_cm_lists(w.col_rows, w.col_signs, s, m, 0, 12, n, (n + 4095) / 4096, w.lists, st)))
     return rc;
   skh_trace_mark(st, "hash_gen");
   const uint64_t dkey = key_diag(seed);
@@ -306,11 +351,15 @@ int hrdht_run(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const d
     if ((rc = launch_dht_pow2(n, d, A, lda, b, dkey, (double2*)w.Z, (double2*)w.tw, w.H, d, w.hb, st))) return rc;
     return finish_rowmajor(seed, n, m, d, w, b, SA, ldsa, Sb, c, sample, st);
   }
-  if (pow2) {  // column-major, n = 2^L >= 256: H = Fhat D [A | b] into Y, then the tile gather
-    if ((rc = launch_dht_pow2_cm(n, d, A, lda, b, dkey, (double2*)w.Z, (double2*)w.tw, w.Y, n, st))) return rc;
-    if ((rc = launch_cm_gather(w.Y, n, ncol, nullptr, n, (n + 4095) / 4096, 12, 0, w.lists, s, m, SA, ldsa, d, Sb, c,
-                               st)))
-      return rc;
+  if (pow2) {  // column-major, n = 2^L: transpose A into H, the row-major passes (H in place), gather, transpose SA
+    transpose_cm_to_rm(n, d, A, lda, w.H, d, st);
+    if ((rc = check_launch("hrdht: transpose"))) return rc;
+    skh_trace_mark(st, "transpose");
+    if ((rc = launch_dht_pow2(n, d, w.H, d, b, dkey, (double2*)w.Z, (double2*)w.tw, w.H, d, w.hb, st))) return rc;
+    if ((rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.H, d, w.SAt, d, c, st))) return rc;
+    if (b && (rc = launch_gather_vec(m, w.ptr, w.rows, w.signs, w.hb, Sb, c, st))) return rc;
+    transpose_cm_to_rm(d, m, w.SAt, d, SA, ldsa, st);  // SA[c * ldsa + b] = SAt[b * d + c]
+    if ((rc = check_launch("hrdht: SA transpose"))) return rc;
     skh_trace_mark(st, "gather");
     return SKH_OK;
   }

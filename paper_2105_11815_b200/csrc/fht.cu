@@ -291,155 +291,6 @@ int dispatch_B(int k, int64_t n2, int64_t d, const double2* Z, int64_t ldz, cons
   }
 }
 
-// ---------------------------------------------------------------- column-major A
-// Column c of A is a contiguous n-vector, j = j1 + n1 j2 with j1 contiguous.
-// cm pass A (CTA = column x 16 consecutive j1): the n2-point DFTs over j2 (rows
-//   of the column's n2 x n1 view, stride n1), two adjacent j1 packed per complex
-//   FFT (one 16-byte load), D fused; times W_n^{j1 k2} (per lane now); written
-//   as Z[c][j1][k2], k2 <= n2/2 contiguous (the epilogue reads the tile from
-//   shared memory in k2-major order, so the stores are coalesced).
-// cm pass B (CTA = column x 8 consecutive k2): the n1-point DFTs over j1 (rows
-//   of Z[c], stride ldzr), H[c][k] = Re - Im for k = k2 + n2 k1 and the mirror
-//   H[c][n - k] = Re + Im for 0 < k2 < n2/2: 8 consecutive k2 = 64-byte runs.
-__device__ __forceinline__ const double* cm_col(const double* X, int64_t ldx, int64_t ncolX, const double* xb,
-                                                int64_t c) {
-  return c < ncolX ? X + c * ldx : xb;
-}
-
-template <int K>
-__global__ void __launch_bounds__(kThreads, 5)
-    dht_cm_passA_kernel(int64_t n1, int64_t ncolX, const double* __restrict__ X, int64_t ldx,
-                        const double* __restrict__ xb, uint64_t dkey, const double2* __restrict__ tw,
-                        double2* __restrict__ Z, int64_t ldzr, int64_t zcol, int64_t jtiles) {
-  constexpr int N = 1 << K, TC = 8, TR = 16;
-  extern __shared__ double2 smem[];
-  double2* z = smem;
-  double2* wN = smem + N * TC;
-  uint32_t* sg = reinterpret_cast<uint32_t*>(wN + N / 2);  // 16 sign bits per j2
-  const int64_t c = blockIdx.x / jtiles, j10 = (blockIdx.x % jtiles) * TR;
-  const double* src = cm_col(X, ldx, ncolX, xb, c) + j10;
-  const bool pairs = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)(n1 * 8)) & 15) == 0;
-  constexpr int A1 = K < 4 ? K : 4, R1 = 1 << A1, p1 = K - A1;
-  constexpr int G1 = (N >> A1) * TC, GPT1 = (G1 + kThreads - 1) / kThreads;
-  double2 pre[GPT1][R1];
-#pragma unroll
-  for (int u = 0; u < GPT1; ++u) {
-    const int g = threadIdx.x + u * kThreads;
-    const int cc = g % TC, rest = g / TC;
-    const int base = (rest & ((1 << p1) - 1)) | ((rest >> p1) << K);
-#pragma unroll
-    for (int t = 0; t < R1; ++t) {
-      const double* a = src + n1 * (base + (t << p1)) + 2 * cc;
-      double2 x = make_double2(0.0, 0.0);
-      if (g < G1) x = pairs ? __ldg(reinterpret_cast<const double2*>(a)) : make_double2(__ldg(a), __ldg(a + 1));
-      pre[u][t] = x;
-    }
-  }
-  const int64_t n = n1 << K;
-  load_wN<K>(wN, tw, n);
-  for (int j2 = threadIdx.x; j2 < N; j2 += kThreads) {  // rows j10 + n1 j2 .. + 15 (16-aligned)
-    const int64_t g0 = j10 + n1 * j2;
-    sg[j2] = (uint32_t)(stream_u(dkey, (uint64_t)(g0 >> 6)) >> (g0 & 63)) & 0xFFFFu;
-  }
-  __syncthreads();
-  dif_rounds<K, TC, K, 4, 4>(
-      z, wN,
-      [&](int u, int t, int i, int cc) {
-        const uint32_t w = sg[i] >> (2 * cc);
-        return make_double2((w & 1u) ? -pre[u][t].x : pre[u][t].x, (w & 2u) ? -pre[u][t].y : pre[u][t].y);
-      },
-      [&](int i, int cc, double2 v) { z[i * TC + cc] = v; });
-  __syncthreads();
-  constexpr int NK = N / 2 + 1;
-  double2* zc = Z + c * zcol;
-  for (int e = threadIdx.x; e < NK * TC; e += kThreads) {
-    // k2 fastest: coalesced stores along Z's rows (packed column fastest, with
-    // conflict-free shared reads but 64-byte store runs, measured slower)
-    const int cc = e / NK, k2 = e % NK;
-    const double2 zk = z[bitrev(k2, K) * TC + cc], zm = z[bitrev((N - k2) & (N - 1), K) * TC + cc];
-    double2 ya = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-    double2 yb = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
-    const int64_t ja = j10 + 2 * cc;
-    if (k2) {
-      if (ja) ya = cmul(ya, tw[ja * k2]);  // j1 k2 <= n/2
-      yb = cmul(yb, tw[(ja + 1) * k2]);
-    }
-    zc[ja * ldzr + k2] = ya;
-    zc[(ja + 1) * ldzr + k2] = yb;
-  }
-}
-
-template <int K>
-__global__ void __launch_bounds__(kThreads, 5)
-    dht_cm_passB_kernel(int64_t n2, const double2* __restrict__ Z, int64_t ldzr, int64_t zcol,
-                        const double2* __restrict__ tw, double* __restrict__ H, int64_t ldh, int64_t ktiles) {
-  constexpr int N = 1 << K, TC = 8;
-  extern __shared__ double2 smem[];
-  double2* z = smem;
-  double2* wN = smem + N * TC;
-  const int64_t n = n2 << K;
-  const int64_t c = blockIdx.x / ktiles, k20 = (blockIdx.x % ktiles) * TC;
-  const double2* src = Z + c * zcol + k20;
-  load_wN<K>(wN, tw, n);
-  __syncthreads();
-  auto ld = [&](int, int, int j1, int cc) { return src[(int64_t)j1 * ldzr + cc]; };
-  double* h = H + c * ldh;
-  dif_rounds<K, TC, K, 4, (K >= 9 ? 5 : 4)>(z, wN, ld, [&](int i, int cc, double2 v) {
-    const int64_t k2 = k20 + cc;
-    if (2 * k2 > n2) return;
-    const int64_t k = k2 + n2 * bitrev(i, K);
-    h[k] = v.x - v.y;
-    if (k2 > 0 && 2 * k2 < n2) h[n - k] = v.x + v.y;
-  });
-}
-
-template <int K>
-int launch_cm_A(int64_t n1, int64_t ncols, int64_t ncolX, const double* X, int64_t ldx, const double* xb,
-                uint64_t dkey, const double2* tw, double2* Z, int64_t ldzr, int64_t zcol, cudaStream_t st) {
-  constexpr int N = 1 << K;
-  const int64_t jtiles = n1 / 16;
-  const size_t sm = sizeof(double2) * (size_t)(N * 8 + N / 2) + sizeof(uint32_t) * N;
-  cudaFuncSetAttribute(dht_cm_passA_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dht_cm_passA_kernel<K><<<(unsigned)(ncols * jtiles), kThreads, sm, st>>>(n1, ncolX, X, ldx, xb, dkey, tw, Z, ldzr,
-                                                                           zcol, jtiles);
-  note_launch();
-  return check_launch("dht cm pass A");
-}
-
-template <int K>
-int launch_cm_B(int64_t n2, int64_t ncols, const double2* Z, int64_t ldzr, int64_t zcol, const double2* tw,
-                double* H, int64_t ldh, cudaStream_t st) {
-  constexpr int N = 1 << K;
-  const int64_t ktiles = (n2 / 2 + 1 + 7) / 8;
-  const size_t sm = sizeof(double2) * (size_t)(N * 8 + N / 2);
-  cudaFuncSetAttribute(dht_cm_passB_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dht_cm_passB_kernel<K><<<(unsigned)(ncols * ktiles), kThreads, sm, st>>>(n2, Z, ldzr, zcol, tw, H, ldh, ktiles);
-  note_launch();
-  return check_launch("dht cm pass B");
-}
-
-template <int K = 1>
-int dispatch_cm_A(int k, int64_t n1, int64_t ncols, int64_t ncolX, const double* X, int64_t ldx, const double* xb,
-                  uint64_t dkey, const double2* tw, double2* Z, int64_t ldzr, int64_t zcol, cudaStream_t st) {
-  if constexpr (K > 9) {
-    return SKH_EINVAL;
-  } else {
-    if (k == K) return launch_cm_A<K>(n1, ncols, ncolX, X, ldx, xb, dkey, tw, Z, ldzr, zcol, st);
-    return dispatch_cm_A<K + 1>(k, n1, ncols, ncolX, X, ldx, xb, dkey, tw, Z, ldzr, zcol, st);
-  }
-}
-
-template <int K = 1>
-int dispatch_cm_B(int k, int64_t n2, int64_t ncols, const double2* Z, int64_t ldzr, int64_t zcol, const double2* tw,
-                  double* H, int64_t ldh, cudaStream_t st) {
-  if constexpr (K > 9) {
-    return SKH_EINVAL;
-  } else {
-    if (k == K) return launch_cm_B<K>(n2, ncols, Z, ldzr, zcol, tw, H, ldh, st);
-    return dispatch_cm_B<K + 1>(k, n2, ncols, Z, ldzr, zcol, tw, H, ldh, st);
-  }
-}
-
 int ilog2(int64_t n) {
   int L = 0;
   while ((1ll << L) < n) ++L;
@@ -477,40 +328,6 @@ int launch_dht_pow2(int64_t n, int64_t d, const double* A, int64_t lda, const do
   if ((rc = dispatch_A(L2, n1, d, A, lda, b, dkey, tw, Z, ldz, st))) return rc;
   skh_trace_mark(st, "dht_passA");
   if ((rc = dispatch_B(L1, n2, d, Z, ldz, tw, H, ldh, b ? hb : nullptr, st))) return rc;
-  skh_trace_mark(st, "dht_passB");
-  return SKH_OK;
-}
-
-// Column-major: n = 2^L with 8 <= L <= 18 (16 <= n1).  The split puts the
-// larger half on the contiguous j1 (pass B).
-bool dht_pow2_cm_supported(int64_t n) { return dht_pow2_supported(n) && n >= 256; }
-
-int64_t dht_pow2_cm_ldzr(int64_t n) {
-  const int L = ilog2(n), L2 = L - split_L1(L);
-  return ((1ll << L2) / 2 + 1 + 7) / 8 * 8;
-}
-
-size_t dht_pow2_cm_z_elems(int64_t n, int64_t ncols) {
-  const int L = ilog2(n), L1 = split_L1(L);
-  return (size_t)(1ll << L1) * (size_t)dht_pow2_cm_ldzr(n) * (size_t)ncols;
-}
-
-// H[c][k] (ldh >= n) = Fhat D X[:, c] for the ncolX columns of X (ldx) and xb
-// as column ncolX when given; unnormalised.
-int launch_dht_pow2_cm(int64_t n, int64_t ncolX, const double* X, int64_t ldx, const double* xb, uint64_t dkey,
-                       double2* Z, double2* tw, double* H, int64_t ldh, cudaStream_t st) {
-  const int L = ilog2(n), L1 = split_L1(L), L2 = L - L1;
-  const int64_t n1 = 1ll << L1, n2 = 1ll << L2;
-  const int64_t ncols = ncolX + (xb ? 1 : 0);
-  const int64_t ldzr = dht_pow2_cm_ldzr(n), zcol = n1 * ldzr;
-  twiddle_kernel<<<(unsigned)((n / 2 + 1 + 255) / 256), 256, 0, st>>>(n, tw);
-  note_launch();
-  int rc = check_launch("dht twiddles");
-  if (rc) return rc;
-  skh_trace_mark(st, "twiddle");
-  if ((rc = dispatch_cm_A(L2, n1, ncols, ncolX, X, ldx, xb, dkey, tw, Z, ldzr, zcol, st))) return rc;
-  skh_trace_mark(st, "dht_passA");
-  if ((rc = dispatch_cm_B(L1, n2, ncols, Z, ldzr, zcol, tw, H, ldh, st))) return rc;
   skh_trace_mark(st, "dht_passB");
   return SKH_OK;
 }
