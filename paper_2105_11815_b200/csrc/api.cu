@@ -89,6 +89,48 @@ cudaStream_t copy_stream() {
   return streams[dev];
 }
 
+// Side stream per device for independent small work (Sb = S b beside S A):
+// fork = the side stream waits for everything already on `st`; join = `st`
+// waits for the side stream.  Events are per thread and device.
+cudaStream_t side_stream() {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+  return streams[dev];
+}
+
+cudaEvent_t side_event(int which) {
+  thread_local cudaEvent_t ev[64][2] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!ev[dev][which]) cudaEventCreateWithFlags(&ev[dev][which], cudaEventDisableTiming);
+  return ev[dev][which];
+}
+
+// returns the stream to launch the side work on (st itself if no side stream)
+cudaStream_t side_fork(cudaStream_t st) {
+  cudaStream_t side = side_stream();
+  cudaEvent_t e = side_event(0);
+  if (!side || !e || cudaEventRecord(e, st) != cudaSuccess || cudaStreamWaitEvent(side, e, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return st;
+  }
+  return side;
+}
+
+int side_join(cudaStream_t st, cudaStream_t side) {
+  if (side == st) return SKH_OK;
+  cudaEvent_t e = side_event(1);
+  if (!e || cudaEventRecord(e, side) != cudaSuccess || cudaStreamWaitEvent(st, e, 0) != cudaSuccess)
+    return check_launch("side stream join");
+  return SKH_OK;
+}
+
 int validate_hash_args(int64_t m, int32_t s, int64_t nrows) {
   if (m < 1 || s < 1 || (int64_t)s > m || s > 64 || nrows < 0) {
     set_error("invalid arguments: need 1 <= s <= m, s <= 64, nrows >= 0 (m=%lld s=%d nrows=%lld)", (long long)m, s,
@@ -299,10 +341,12 @@ int skh_sketch_dense(int64_t m, int32_t s, const int32_t* bucket_ptr, const int3
     return SKH_EDIM;
   }
   cudaStream_t st = as_stream(stream);
+  // Sb (latency-bound, one warp per bucket) on the side stream beside S A
+  cudaStream_t side = b ? side_fork(st) : st;
+  if (b && (rc = launch_gather_vec(m, bucket_ptr, bucket_rows, bucket_signs, b, Sb, alpha, side))) return rc;
   rc = launch_gather_dense(m, bucket_ptr, bucket_rows, bucket_signs, d, A, lda, SA, ldsa, alpha, st);
   if (rc) return rc;
-  if (b) rc = launch_gather_vec(m, bucket_ptr, bucket_rows, bucket_signs, b, Sb, alpha, st);
-  return rc;
+  return b ? side_join(st, side) : SKH_OK;
 }
 
 size_t skh_sketch_csr_workspace_bytes(int64_t nrows, int32_t s, int64_t nnz) {
@@ -334,11 +378,12 @@ int skh_sketch_csr(int64_t m, int32_t s, const int32_t* bucket_ptr, const int32_
     return SKH_EWORKSPACE;
   }
   cudaStream_t st = as_stream(stream);
+  cudaStream_t side = b ? side_fork(st) : st;  // Sb beside the expand + reduce of S A
+  if (b && (rc = launch_gather_vec(m, bucket_ptr, bucket_rows, bucket_signs, b, Sb, alpha, side))) return rc;
   rc = launch_gather_csr(m, s, bucket_ptr, bucket_rows, bucket_signs, nrows, d, nnz, row_ptr, col_idx, val, SA, ldsa,
                          alpha, ws, st);
   if (rc) return rc;
-  if (b) rc = launch_gather_vec(m, bucket_ptr, bucket_rows, bucket_signs, b, Sb, alpha, st);
-  return rc;
+  return b ? side_join(st, side) : SKH_OK;
 }
 
 size_t skh_rht_stages_workspace_bytes(int64_t nrows, int64_t nvalid, int64_t row0, int64_t d) {
