@@ -133,3 +133,27 @@ def test_csr_reduce_paths(case):
                               torch.from_numpy(v).cuda(), d, torch.from_numpy(b).cuda())
     SAo, Sbo = sketch.sketch_csr(17, rp, ci, v, d, b, m, s)
     assert bits(np_(SA), SAo) and bits(np_(Sb), Sbo)
+
+
+def test_side_stream_join_orders_sb():
+    """skh_sketch_dense / skh_sketch_csr compute Sb on a library side stream;
+    the join must order it before later work on the caller's stream (here a
+    non-default torch stream that copies Sb right after the call, 20 times)."""
+    from oracle import sketch
+    n, d, m, s = 20000, 40, 3000, 2
+    r = np.random.default_rng(11)
+    A = r.standard_normal((n, d))
+    bs = [r.standard_normal(n) for _ in range(4)]
+    _, Sbo = zip(*[sketch.sketch_dense(6, A[:, :1], bv, m, s) for bv in bs])
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        bl = skh().hash_gen(6, m, s, n)
+        Ad = torch.from_numpy(A).cuda()
+        outs = []
+        for k in range(20):
+            bd = torch.from_numpy(bs[k % 4]).cuda()
+            SA, Sb = skh().sketch_dense(bl, Ad, bd)
+            outs.append(Sb.clone())  # enqueued on st right after the call
+    st.synchronize()
+    for k, o in enumerate(outs):
+        assert bits(np_(o), Sbo[k % 4])
