@@ -33,7 +33,7 @@ constexpr int kTileMax = 4096;   // fp64 accumulator columns per pass (32 KiB)
 constexpr int kChunk = 2048;     // pairs held in registers (8 per thread)
 constexpr int kPer = 2048 / 256;
 constexpr int kFree = 0x7fffffff;
-constexpr int kSideCap = 512;    // side list (pairs of columns with >= 3) per tile
+constexpr int kSideCap = 256;    // side list (pairs of columns with >= 3) per tile
 
 
 struct CsrWs {
@@ -166,7 +166,7 @@ __device__ __forceinline__ void claim_rounds(double* acc, int* claim, const int 
 //     barriers per tile instead of three per round.
 //   fallback (side list over capacity, or a run longer than kChunk): claim
 //     rounds, chunk by chunk.
-__global__ void __launch_bounds__(kThreads, 3) csr_reduce_kernel(
+__global__ void __launch_bounds__(kThreads, 4) csr_reduce_kernel(
     int64_t m, const int32_t* __restrict__ ptr, const int32_t* __restrict__ off, const int32_t* __restrict__ ecol,
     const double* __restrict__ eval, int64_t d, int tile_cols, double* __restrict__ SA, int64_t ldsa, double alpha) {
   extern __shared__ double acc[];  // [tile_cols]
