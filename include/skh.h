@@ -299,16 +299,19 @@ int skh_rht_colmajor(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0,
  * HR-DHT (eq. eqn::HR-DHT, "(6.1)", L1066-1075): SA = S_h F D A, Sb = S_h F D b
  * with F the normalised Discrete Hartley Transform, F_ij = n^{-1/2}
  * [cos + sin](2 pi (i-1)(j-1)/n) -- the sketch of the paper's Ski-LLS-dense.
- * Any n (no padding): S_h hashes the n rows.  The transform is cuFFT's D2Z
- * (Fhat y = Re X - Im X), its work area taken from `ws`; SA = c * (ascending-
- * row signed sums of Fhat D A rows), c = 1/sqrt(n s) (R20).  FFT
- * rounding differs from the oracle's: compared to 1e-12 relative Frobenius.
+ * Any n (no padding): S_h hashes the n rows.  Fhat y = Re X - Im X of the DFT
+ * X of each column: for n = 2^L <= 2^18 the library's own two-pass four-step
+ * transform (column-major A is transposed into the workspace first; DESIGN.md
+ * §5d), otherwise cuFFT's D2Z with its work area taken from `ws`.  SA = c *
+ * (ascending-row signed sums of Fhat D A rows), c = 1/sqrt(n s) (R20).
+ * FFT rounding differs from the oracle's: compared to 1e-12 relative Frobenius.
  *   skh_hrdht_dense:          A row-major [n x d] (lda >= d), SA [m x d] (ldsa >= d), s <= 64
  *   skh_hrdht_dense_colmajor: A column-major (lda >= n), SA column-major (ldsa >= m),
  *                             s <= 8, m <= 65536
- * b nullable, Sb required iff b.  ws: the matching query (holds two transformed
- * copies of [A b]; creating the cuFFT plan needs the device).  cuFFT plans are
- * cached per host thread, device, n and batch for the life of the process. */
+ * b nullable, Sb required iff b.  ws: the matching query (about two transformed
+ * copies of [A b]; for the cuFFT sizes creating the plan needs the device).
+ * cuFFT plans are cached per host thread, device, n and batch for the life of
+ * the process. */
 size_t skh_hrdht_dense_workspace_bytes(int64_t n, int64_t m, int32_t s, int64_t d);
 int skh_hrdht_dense(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d,
                     const double* A, int64_t lda, const double* b,
