@@ -231,6 +231,19 @@ def roofline(cfg, step, stage_ms, peak_gbs, peak_src, layout="row", sketch="hash
                 "peak": peak_gbs, "unit": "GB/s", "frac": round(ach / peak_gbs, 4), "traffic": None,
                 "traffic_source": None, "alg_bytes_per_launch": alg[name], "ms_per_launch": round(t, 4),
                 "peak_source": peak_src}
+    if layout == "col" and "transpose" in stage_ms:
+        # plain column-major sketch with the transposed path (skh.h): the tiled
+        # transpose reads + writes A once; the row gather reads the copy once,
+        # writes SA, and SA is transposed out (read + write)
+        nb = cfg.n * cfg.d * 8
+        alg = {"transpose": 2 * nb, "gather": nb + 3 * cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5}
+        label = {"transpose": "cm_to_rm_kernel (A transpose)", "gather": "gather_wide + SA transpose"}
+        name = max((k for k in stage_ms if k in alg), key=lambda k: stage_ms[k])
+        t = stage_ms[name]
+        achieved = alg[name] / (t / 1e3) / 1e9
+        return {"bound": "hbm", "kernel": label[name], "achieved": round(achieved, 1), "peak": peak_gbs,
+                "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": None, "traffic_source": None,
+                "alg_bytes_per_launch": alg[name], "ms_per_launch": round(t, 4), "peak_source": peak_src}
     if layout == "col":
         # dominant by time; algorithmic bytes of each kernel per launch:
         #  pass1: read + write (d + 1) columns of n_pad rows once

@@ -53,6 +53,7 @@ SIGNATURES = {
     "skh_rht_dense_colmajor_host": (ctypes.c_int, [c_u64, c_i64, c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_p, c_i64,
                                                    c_p, c_p, c_sz, c_p]),
     "skh_sketch_dense_colmajor_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32]),
+    "skh_sketch_dense_colmajor_fast_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32, c_i64]),
     "skh_sketch_dense_colmajor": (ctypes.c_int, [c_u64, c_i64, c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_p, c_i64, c_p,
                                                  c_p, c_sz, c_p]),
     "skh_rht_colmajor": (ctypes.c_int, [c_u64, c_i64, c_i64, c_i64, c_i64, c_p, c_i64, c_p, c_i64, ctypes.c_int,

@@ -334,8 +334,10 @@ def rht_dense_colmajor(seed, At, b, m, s):
     return RhtDenseColMajor(n, m, s, d, At.device)(seed, At, b)
 
 
-def sketch_dense_colmajor(seed, At, b, m, s, SAt=None, Sb=None, ws=None):
-    """Plain s-hashing SA = S A of column-major A (At: (d, n)); bit-identical to sketch_dense."""
+def sketch_dense_colmajor(seed, At, b, m, s, SAt=None, Sb=None, ws=None, fast=True):
+    """Plain s-hashing SA = S A of column-major A (At: (d, n)); bit-identical to sketch_dense.
+    fast=True sizes the workspace for the transposed path (a row-major copy of A),
+    fast=False for the on-chip walk (skh.h)."""
     lib = _lib.load()
     _need_cuda(At, b)
     d, n = At.shape
@@ -344,7 +346,9 @@ def sketch_dense_colmajor(seed, At, b, m, s, SAt=None, Sb=None, ws=None):
     if b is not None and Sb is None:
         Sb = torch.empty(m, dtype=torch.float64, device=At.device)
     if ws is None:
-        ws = _workspace(lib.skh_sketch_dense_colmajor_workspace_bytes(n, m, s), At.device)
+        nb = (lib.skh_sketch_dense_colmajor_fast_workspace_bytes(n, m, s, d) if fast
+              else lib.skh_sketch_dense_colmajor_workspace_bytes(n, m, s))
+        ws = _workspace(nb, At.device)
     rc = lib.skh_sketch_dense_colmajor(int(seed) & (2**64 - 1), n, int(m), int(s), d, _ptr(At), _ld_cm(At, n),
                                        _ptr(b), _ptr(SAt), _ld_cm(SAt, m), _ptr(Sb), _ptr(ws), ws.numel(), _stream())
     _lib.check(rc, "skh_sketch_dense_colmajor")

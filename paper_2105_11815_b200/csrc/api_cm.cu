@@ -304,12 +304,48 @@ int skh_rht_dense_colmajor_host(uint64_t seed, int64_t n, int64_t m, int32_t s, 
   return rc;
 }
 
+// Transposed path of skh_sketch_dense_colmajor: bucket lists, A^T into a
+// row-major copy, the row gather into a row-major SA, SA transposed out.
+struct CmFastWs {
+  int32_t* ptr;
+  int32_t* rows;
+  int8_t* signs;
+  void* hws;
+  double* Arm;  // [n x d] row-major copy of A
+  double* SAt;  // [m x d] row-major SA
+  size_t total;
+};
+
+CmFastWs cm_fast_layout(void* base, int64_t n, int64_t m, int s, int64_t d) {
+  CmFastWs w{};
+  char* p = static_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* q = p ? p + off : nullptr;
+    off += align_up(bytes);
+    return q;
+  };
+  w.ptr = (int32_t*)take(sizeof(int32_t) * (size_t)(m + 1));
+  w.rows = (int32_t*)take(sizeof(int32_t) * (size_t)n * s);
+  w.signs = (int8_t*)take((size_t)n * s);
+  w.hws = take(hash_ws_bytes(n, m, s));
+  w.Arm = (double*)take(sizeof(double) * (size_t)n * (size_t)d);
+  w.SAt = (double*)take(sizeof(double) * (size_t)m * (size_t)d);
+  w.total = off;
+  return w;
+}
+
 size_t skh_sketch_dense_colmajor_workspace_bytes(int64_t n, int64_t m, int32_t s) {
   if (n < 1 || m < 1 || s < 1) return 0;
   const CmPlan pl = cm_plan(n);  // K2 = 0 tiles for any n (only ntiles is used)
   const int64_t ntiles = (n + (1 << kCmTile) - 1) >> kCmTile;
   (void)pl;
   return cm_layout(nullptr, n, 0, 0, m, s, 1, ntiles, false).total;
+}
+
+size_t skh_sketch_dense_colmajor_fast_workspace_bytes(int64_t n, int64_t m, int32_t s, int64_t d) {
+  if (n < 1 || m < 1 || s < 1 || d < 1) return 0;
+  return std::max(cm_fast_layout(nullptr, n, m, s, d).total, skh_sketch_dense_colmajor_workspace_bytes(n, m, s));
 }
 
 int skh_sketch_dense_colmajor(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const double* A,
@@ -324,6 +360,27 @@ int skh_sketch_dense_colmajor(uint64_t seed, int64_t n, int64_t m, int32_t s, in
   if (lda < n || ldsa < m || (b && !Sb)) {
     set_error("sketch_dense_colmajor: need lda >= n, ldsa >= m, Sb when b is given");
     return SKH_EDIM;
+  }
+  if (ws && ws_bytes >= cm_fast_layout(nullptr, n, m, s, d).total) {
+    // the workspace holds a row-major copy: transpose, row gather (bit-identical:
+    // the same ascending-row sums), transpose SA back
+    const CmFastWs f = cm_fast_layout(ws, n, m, s, d);
+    cudaStream_t st = as_stream(stream);
+    trace_begin(st);
+    rc = launch_hash(seed, m, s, n, 0, 0, 0, nullptr, nullptr, f.ptr, f.rows, f.signs, f.hws, hash_ws_bytes(n, m, s),
+                     st);
+    if (rc) return rc;
+    skh_trace_mark(st, "hash_gen");
+    transpose_cm_to_rm(n, d, A, lda, f.Arm, d, st);
+    if ((rc = check_launch("sketch_dense_colmajor: transpose"))) return rc;
+    skh_trace_mark(st, "transpose");
+    const double c = skh_c_s(s);
+    if ((rc = launch_gather_dense(m, f.ptr, f.rows, f.signs, d, f.Arm, d, f.SAt, d, c, st))) return rc;
+    if (b && (rc = launch_gather_vec(m, f.ptr, f.rows, f.signs, b, Sb, c, st))) return rc;
+    transpose_cm_to_rm(d, m, f.SAt, d, SA, ldsa, st);
+    if ((rc = check_launch("sketch_dense_colmajor: SA transpose"))) return rc;
+    skh_trace_mark(st, "gather");
+    return SKH_OK;
   }
   CmPlan pl{};
   pl.K2 = 0;

@@ -48,6 +48,9 @@ void note_launch();
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Kernel launchers (one per .cu file).
+// dht.cu: Y[i * ldy + c] = X[c * ldx + i] (column-major n x d -> row-major), 64 x 64 tiles
+void transpose_cm_to_rm(int64_t n, int64_t d, const double* X, int64_t ldx, double* Y, int64_t ldy, cudaStream_t st);
+
 // hash.cu
 size_t hash_ws_bytes(int64_t nrows, int64_t m, int s);
 int launch_hash(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, int64_t blk,

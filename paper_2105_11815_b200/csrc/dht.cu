@@ -41,42 +41,10 @@ size_t dht_pow2_z_elems(int64_t n, int64_t ncol);
 int launch_dht_pow2(int64_t n, int64_t d, const double* A, int64_t lda, const double* b, uint64_t dkey,
                     double2* Z, double2* tw, double* H, int64_t ldh, double* hb, cudaStream_t st);
 
-namespace {
-
-// n = 2^L (4 <= n <= 2^18) takes the fht.cu passes -- column-major A through a
-// tiled transpose first -- unless SKH_DHT_CUFFT=1 (kept for comparison: D +
-// layout change, cuFFT D2Z, Hartley combine).
-bool use_pow2(int64_t n, bool rowmajor) {
-  static const bool force_cufft = [] {
-    const char* e = getenv("SKH_DHT_CUFFT");
-    return e && e[0] == '1';
-  }();
-  return !force_cufft && dht_pow2_supported(n);
-}
-
-__device__ __forceinline__ double dsign(uint64_t dkey, int64_t g) {
-  return ((stream_u(dkey, (uint64_t)(g >> 6)) >> (g & 63)) & 1ull) ? -1.0 : 1.0;
-}
-
-// Y[c * n + i] = D_i A[i, c] (row-major A, lda) for c < d; Y[d * n + i] = D_i b[i]
-__global__ void diag_transpose_kernel(int64_t n, int64_t d, const double* __restrict__ A, int64_t lda,
-                                      double* __restrict__ Y, uint64_t dkey) {
-  __shared__ double tile[32][33];
-  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
-  for (int k = threadIdx.y; k < 32; k += 8) {
-    const int64_t r = r0 + k, c = c0 + threadIdx.x;
-    tile[k][threadIdx.x] = (r < n && c < d) ? A[r * lda + c] : 0.0;
-  }
-  __syncthreads();
-  for (int k = threadIdx.y; k < 32; k += 8) {
-    const int64_t c = c0 + k, r = r0 + threadIdx.x;
-    if (r < n && c < d) Y[c * n + r] = dsign(dkey, r) * tile[threadIdx.x][k];
-  }
-}
-
 // Y[i * ldy + c] = X[c * ldx + i]: column-major n x d -> row-major, 64 x 64
 // tiles, 16-byte accesses on both sides when X, Y and the strides are even
 // (512 bytes per warp instruction), 2-way shared-memory conflicts at most.
+namespace {
 template <bool V2>
 __global__ void __launch_bounds__(256) cm_to_rm_kernel(int64_t n, int64_t d, const double* __restrict__ X,
                                                        int64_t ldx, double* __restrict__ Y, int64_t ldy) {
@@ -111,6 +79,8 @@ __global__ void __launch_bounds__(256) cm_to_rm_kernel(int64_t n, int64_t d, con
   }
 }
 
+}  // namespace
+
 void transpose_cm_to_rm(int64_t n, int64_t d, const double* X, int64_t ldx, double* Y, int64_t ldy, cudaStream_t st) {
   const bool v2 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) % 16 == 0) && ldx % 2 == 0 &&
                   ldy % 2 == 0;
@@ -118,6 +88,39 @@ void transpose_cm_to_rm(int64_t n, int64_t d, const double* X, int64_t ldx, doub
   if (v2) cm_to_rm_kernel<true><<<g, 256, 0, st>>>(n, d, X, ldx, Y, ldy);
   else cm_to_rm_kernel<false><<<g, 256, 0, st>>>(n, d, X, ldx, Y, ldy);
   note_launch();
+}
+
+namespace {
+
+// n = 2^L (4 <= n <= 2^18) takes the fht.cu passes -- column-major A through a
+// tiled transpose first -- unless SKH_DHT_CUFFT=1 (kept for comparison: D +
+// layout change, cuFFT D2Z, Hartley combine).
+bool use_pow2(int64_t n, bool rowmajor) {
+  static const bool force_cufft = [] {
+    const char* e = getenv("SKH_DHT_CUFFT");
+    return e && e[0] == '1';
+  }();
+  return !force_cufft && dht_pow2_supported(n);
+}
+
+__device__ __forceinline__ double dsign(uint64_t dkey, int64_t g) {
+  return ((stream_u(dkey, (uint64_t)(g >> 6)) >> (g & 63)) & 1ull) ? -1.0 : 1.0;
+}
+
+// Y[c * n + i] = D_i A[i, c] (row-major A, lda) for c < d; Y[d * n + i] = D_i b[i]
+__global__ void diag_transpose_kernel(int64_t n, int64_t d, const double* __restrict__ A, int64_t lda,
+                                      double* __restrict__ Y, uint64_t dkey) {
+  __shared__ double tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int64_t r = r0 + k, c = c0 + threadIdx.x;
+    tile[k][threadIdx.x] = (r < n && c < d) ? A[r * lda + c] : 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int64_t c = c0 + k, r = r0 + threadIdx.x;
+    if (r < n && c < d) Y[c * n + r] = dsign(dkey, r) * tile[threadIdx.x][k];
+  }
 }
 
 // Y[c * n + i] = D_i X[c * ldx + i] (column-major X) for c < ncol

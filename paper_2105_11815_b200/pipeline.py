@@ -175,7 +175,7 @@ class ColStep:
             self.op = api.RhtDenseColMajor(n, m, s, d, dev)
         else:
             lib = api._lib.load()
-            self.ws = api._workspace(lib.skh_sketch_dense_colmajor_workspace_bytes(n, m, s), dev)
+            self.ws = api._workspace(lib.skh_sketch_dense_colmajor_fast_workspace_bytes(n, m, s, d), dev)
         self.record = record
 
     def new_timer(self):

@@ -266,3 +266,22 @@ def test_determinism_stress_shared_memory_paths():
             assert torch.equal(SA, rr[0][0])
             if Sb is not None:
                 assert torch.equal(Sb, rr[0][1])
+
+
+@pytest.mark.parametrize("n,d,m,s", [(5000, 3, 300, 2), (4096 * 3 + 17, 70, 1000, 1), (9000, 129, 64, 8)])
+def test_plain_colmajor_fast_and_walk_bit_identical(n, d, m, s):
+    """skh_sketch_dense_colmajor's two paths (transpose + row gather when the
+    workspace has room for a row-major copy, else the on-chip walk) are both
+    bit-identical to the oracle."""
+    import numpy as np
+    from oracle import sketch
+    r = np.random.default_rng(n + d)
+    A = r.standard_normal((n, d))
+    b = r.standard_normal(n)
+    At = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    bd = torch.from_numpy(b).cuda()
+    SAo, Sbo = sketch.sketch_dense(5, A, b, m, s)
+    for fast in (True, False):
+        SAt, Sb = skh().sketch_dense_colmajor(5, At, bd, m, s, fast=fast)
+        assert np.array_equal(SAt.cpu().numpy().T.view(np.int64), SAo.view(np.int64))
+        assert np.array_equal(Sb.cpu().numpy().view(np.int64), Sbo.view(np.int64))
