@@ -157,3 +157,15 @@ def test_side_stream_join_orders_sb():
     st.synchronize()
     for k, o in enumerate(outs):
         assert bits(np_(o), Sbo[k % 4])
+
+
+def test_colmajor_paths_without_b():
+    """The transposed column-major paths (plain sketch, HR-DHT) with b = None."""
+    from oracle import hartley, sketch
+    n, d, m, s = 4096, 33, 500, 2
+    A = np.random.default_rng(21).standard_normal((n, d))
+    At = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    SAt, Sb = skh().sketch_dense_colmajor(3, At, None, m, s)
+    assert Sb is None and bits(np_(SAt).T, sketch.sketch_dense(3, A, None, m, s)[0])
+    SAt, Sb = skh().hrdht_dense_colmajor(3, At, None, m, s)
+    assert Sb is None and rel(np_(SAt).T, hartley.hrdht_sketch(3, A, None, m, s)[0]) <= TOL
