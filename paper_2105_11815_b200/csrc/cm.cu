@@ -439,6 +439,132 @@ __global__ void __launch_bounds__(256 * NC, 2 / NC) cm_pass2_kernel(const PassAr
   }
 }
 
+// Warp-specialised pass 2 (GATHER, one column per CTA at a time, 512 threads):
+// warps 0-7 produce -- load a tile, butterflies, the final values into tile
+// buffer b (and the tile's list into list buffer b) -- while warps 8-15 consume
+// the other buffer with the rank rounds.  The halves meet only at named
+// barriers: FULL[b] (producers arrive, consumers wait) and EMPTY[b] (consumers
+// arrive, producers wait); the exchange and the rank rounds each use a barrier
+// of their own half.  Same arithmetic and order as cm_pass2_kernel.
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+constexpr int kBarProd = 1, kBarCons = 2, kBarFull = 3, kBarEmpty = 5;
+constexpr int kRoffPad = 48;
+
+__host__ __device__ constexpr size_t ws_smem_bytes(int s, int nb) {
+  return 2 * (size_t)kE * 8 + 2 * (size_t)4 * list_cap(s) + 2 * sizeof(int32_t) * kRoffPad + 8 * (size_t)nb;
+}
+
+template <int K2>
+__global__ void __launch_bounds__(512, 1) cm_pass2_ws_kernel(const PassArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int cap = list_cap(a.s);
+  double* buf = reinterpret_cast<double*>(smraw);                                   // [2][kE]
+  uint32_t* lst = reinterpret_cast<uint32_t*>(smraw + 2 * (size_t)kE * 8);          // [2][cap]
+  int32_t* ro = reinterpret_cast<int32_t*>(smraw + 2 * (size_t)kE * 8 + 2 * (size_t)4 * cap);  // [2][kRoffPad]
+  double* sa = reinterpret_cast<double*>(smraw + 2 * (size_t)kE * 8 + 2 * (size_t)4 * cap +
+                                         2 * sizeof(int32_t) * kRoffPad);  // [nb]
+  const int tid = threadIdx.x, t = tid & 255;
+  const bool producer = tid < 256;
+  const int64_t my_cols = a.ncols > blockIdx.x ? (a.ncols - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t nitems = my_cols * a.ntiles;
+  auto col_of = [&](int64_t i) { return (int64_t)blockIdx.x + (i / a.ntiles) * gridDim.x; };
+  if (producer) {
+    double x[16], xn[16];
+    if (nitems > 0) load_tile<K2>(a, col_of(0), 0, t, xn);
+    for (int64_t i = 0; i < nitems; ++i) {
+      const int b = (int)(i & 1);
+      const int64_t tt = i % a.ntiles;
+#pragma unroll
+      for (int v = 0; v < 16; ++v) x[v] = xn[v];
+      if (i + 1 < nitems) load_tile<K2>(a, col_of(i + 1), (i + 1) % a.ntiles, t, xn);
+      phase0_stages<K2>(x);
+      if (i >= 2) nbar_sync(kBarEmpty + b, 512);  // the consumers are done with buffer b
+      double* ex = buf + (size_t)b * kE;
+      // this tile's list and round offsets into list buffer b
+      const uint4* gl = reinterpret_cast<const uint4*>(a.lists + tt * (int64_t)cap);
+      uint32_t* dl = lst + (size_t)b * cap;
+      for (int k = t; k < cap / 4; k += 256) {
+        const unsigned dsts = (unsigned)__cvta_generic_to_shared(dl + 4 * k);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dsts), "l"(gl + k));
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+      if (t < kRounds + 1) ro[b * kRoffPad + t] = a.roff[tt * kRoffStride + t];
+      if constexpr (K2 > 4) {
+#pragma unroll
+        for (int v = 0; v < 16; ++v) ex[Geo<K2>::p0(t, v)] = x[v];
+        nbar_sync(kBarProd, 256);
+#pragma unroll
+        for (int v = 0; v < 16; ++v) x[v] = ex[Geo<K2>::p1(t, v)];
+        phase1_stages<K2>(x);
+        nbar_sync(kBarProd, 256);  // exchange reads done before the final values overwrite it
+      }
+#pragma unroll
+      for (int v = 0; v < 16; ++v) ex[Geo<K2>::pf(t, v)] = x[v];
+      asm volatile("cp.async.wait_all;\n" ::);
+      nbar_arrive(kBarFull + b, 512);
+    }
+  } else {
+    for (int64_t i = 0; i < nitems; ++i) {
+      const int b = (int)(i & 1);
+      const int64_t tt = i % a.ntiles, col = col_of(i);
+      if (tt == 0) {
+        for (int k = t; k < a.nb; k += 256) sa[k] = 0.0;
+        nbar_sync(kBarCons, 256);
+      }
+      nbar_sync(kBarFull + b, 512);
+      const double* tile = buf + (size_t)b * kE;
+      const uint32_t* slst = lst + (size_t)b * cap;
+      const int32_t* sroff = ro + b * kRoffPad;
+      for (int rho = 0; rho < kRounds; ++rho) {
+        const int e0 = sroff[rho], e1 = sroff[rho + 1];
+        if (e0 == e1) break;
+        if (rho < kRounds - 1) {
+          constexpr int kU = 4;
+          for (int e = e0 + t; e < e1; e += kU * 256) {
+            uint32_t w[kU];
+            int bk[kU];
+            double v[kU], acc[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const int eu = e + u * 256;
+              w[u] = eu < e1 ? slst[eu] : kPadWord;
+              bk[u] = (int)((w[u] >> kLE) & ((1u << kBucketBits) - 1)) - a.b0;
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              if ((unsigned)bk[u] < (unsigned)a.nb) {
+                v[u] = tile[w[u] & (kE - 1)];
+                acc[u] = sa[bk[u]];
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+              if ((unsigned)bk[u] < (unsigned)a.nb) sa[bk[u]] = (w[u] >> 31) ? acc[u] - v[u] : acc[u] + v[u];
+          }
+        } else if (t == 0) {
+          for (int e = e0; e < e1; ++e) {
+            const uint32_t w = slst[e];
+            const int bk = (int)((w >> kLE) & ((1u << kBucketBits) - 1)) - a.b0;
+            if ((unsigned)bk < (unsigned)a.nb) sa[bk] = (w >> 31) ? sa[bk] - tile[w & (kE - 1)] : sa[bk] + tile[w & (kE - 1)];
+          }
+        }
+        nbar_sync(kBarCons, 256);
+      }
+      if (i + 2 < nitems) nbar_arrive(kBarEmpty + b, 512);  // buffer b free (no arrival left unmatched)
+      if (tt == a.ntiles - 1) {  // column done: SA column out (the last round ended with a consumer barrier)
+        if (col < a.ncols) {
+          double* o = col < a.ncolSA ? a.SA + col * a.ldsa : a.Sb;
+          for (int k = t; k < a.nb; k += 256) o[a.b0 + k] = a.alpha * sa[k];
+        }
+        nbar_sync(kBarCons, 256);  // sa is zeroed for the next column
+      }
+    }
+  }
+}
+
 int g_nsm = 0;
 int num_sms() {
   if (!g_nsm) {
@@ -711,8 +837,35 @@ __global__ void cm_lists_par_kernel(const int32_t* __restrict__ col_rows, const 
   }
 }
 
+// Warp-specialised pass 2 where it measured faster: C3HD (K2 = 4, s = 2) pass 2
+// 4.48 -> 3.39 ms; C2 (K2 = 3, s = 1) equal; C5 (K2 = 8, s = 1) 38.5 -> 39.4 ms,
+// so the 8-bit exchange case keeps the two-CTA kernel.  SKH_CM_WS=0/1 forces.
+bool use_ws(int K2, int s) {
+  static const int forced = [] {
+    const char* e = getenv("SKH_CM_WS");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  return forced >= 0 ? forced == 1 : (K2 <= 4 || s >= 2);
+}
+
+template <int K2>
+int launch_pass2_ws(const PassArgs& a, cudaStream_t st) {
+  const size_t smem = ws_smem_bytes(a.s, a.nb);
+  auto* f = cm_pass2_ws_kernel<K2>;
+  int rc = set_smem(f, smem);
+  if (rc) return rc;
+  const int64_t grid = std::min<int64_t>(a.ncols, (int64_t)num_sms());
+  if (grid < 1) return SKH_OK;
+  f<<<(unsigned)grid, 512, smem, st>>>(a);
+  note_launch();
+  return check_launch("cm_pass2_ws");
+}
+
 template <int K2, bool GATHER, int NC>
 int launch_pass2_nc(const PassArgs& a, cudaStream_t st) {
+  if constexpr (GATHER && NC == 1) {
+    if (use_ws(K2, a.s) && ws_smem_bytes(a.s, a.nb) <= 227 * 1024) return launch_pass2_ws<K2>(a, st);
+  }
   const size_t tileb = (size_t)NC * kE * 8;
   const size_t smem = GATHER ? tileb + 256 + (size_t)4 * list_cap(a.s) + 8 * NC * (size_t)a.nb : tileb;
   auto* f = cm_pass2_kernel<K2, GATHER, NC>;
