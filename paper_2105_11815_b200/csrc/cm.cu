@@ -451,14 +451,20 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 constexpr int kBarProd = 1, kBarCons = 2, kBarFull = 3, kBarEmpty = 5;
+// consumer threads: 384 measured slower than 256 (C3HD pass 2 3.52 vs 3.39 ms,
+// C5 40.8 vs 39.4 ms) -- the halves share the shared-memory pipe, not threads
+#ifndef SKH_WS_CONS
+#define SKH_WS_CONS 256
+#endif
 constexpr int kRoffPad = 48;
 
 __host__ __device__ constexpr size_t ws_smem_bytes(int s, int nb) {
   return 2 * (size_t)kE * 8 + 2 * (size_t)4 * list_cap(s) + 2 * sizeof(int32_t) * kRoffPad + 8 * (size_t)nb;
 }
 
-template <int K2>
-__global__ void __launch_bounds__(512, 1) cm_pass2_ws_kernel(const PassArgs a) {
+template <int K2, int CONS>
+__global__ void __launch_bounds__(256 + CONS, 1) cm_pass2_ws_kernel(const PassArgs a) {
+  constexpr int NALL = 256 + CONS;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int cap = list_cap(a.s);
   double* buf = reinterpret_cast<double*>(smraw);                                   // [2][kE]
@@ -466,8 +472,9 @@ __global__ void __launch_bounds__(512, 1) cm_pass2_ws_kernel(const PassArgs a) {
   int32_t* ro = reinterpret_cast<int32_t*>(smraw + 2 * (size_t)kE * 8 + 2 * (size_t)4 * cap);  // [2][kRoffPad]
   double* sa = reinterpret_cast<double*>(smraw + 2 * (size_t)kE * 8 + 2 * (size_t)4 * cap +
                                          2 * sizeof(int32_t) * kRoffPad);  // [nb]
-  const int tid = threadIdx.x, t = tid & 255;
+  const int tid = threadIdx.x;
   const bool producer = tid < 256;
+  const int t = producer ? tid : tid - 256;
   const int64_t my_cols = a.ncols > blockIdx.x ? (a.ncols - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t nitems = my_cols * a.ntiles;
   auto col_of = [&](int64_t i) { return (int64_t)blockIdx.x + (i / a.ntiles) * gridDim.x; };
@@ -481,7 +488,7 @@ __global__ void __launch_bounds__(512, 1) cm_pass2_ws_kernel(const PassArgs a) {
       for (int v = 0; v < 16; ++v) x[v] = xn[v];
       if (i + 1 < nitems) load_tile<K2>(a, col_of(i + 1), (i + 1) % a.ntiles, t, xn);
       phase0_stages<K2>(x);
-      if (i >= 2) nbar_sync(kBarEmpty + b, 512);  // the consumers are done with buffer b
+      if (i >= 2) nbar_sync(kBarEmpty + b, NALL);  // the consumers are done with buffer b
       double* ex = buf + (size_t)b * kE;
       // this tile's list and round offsets into list buffer b
       const uint4* gl = reinterpret_cast<const uint4*>(a.lists + tt * (int64_t)cap);
@@ -504,17 +511,17 @@ __global__ void __launch_bounds__(512, 1) cm_pass2_ws_kernel(const PassArgs a) {
 #pragma unroll
       for (int v = 0; v < 16; ++v) ex[Geo<K2>::pf(t, v)] = x[v];
       asm volatile("cp.async.wait_all;\n" ::);
-      nbar_arrive(kBarFull + b, 512);
+      nbar_arrive(kBarFull + b, NALL);
     }
   } else {
     for (int64_t i = 0; i < nitems; ++i) {
       const int b = (int)(i & 1);
       const int64_t tt = i % a.ntiles, col = col_of(i);
       if (tt == 0) {
-        for (int k = t; k < a.nb; k += 256) sa[k] = 0.0;
-        nbar_sync(kBarCons, 256);
+        for (int k = t; k < a.nb; k += CONS) sa[k] = 0.0;
+        nbar_sync(kBarCons, CONS);
       }
-      nbar_sync(kBarFull + b, 512);
+      nbar_sync(kBarFull + b, NALL);
       const double* tile = buf + (size_t)b * kE;
       const uint32_t* slst = lst + (size_t)b * cap;
       const int32_t* sroff = ro + b * kRoffPad;
@@ -523,13 +530,13 @@ __global__ void __launch_bounds__(512, 1) cm_pass2_ws_kernel(const PassArgs a) {
         if (e0 == e1) break;
         if (rho < kRounds - 1) {
           constexpr int kU = 4;
-          for (int e = e0 + t; e < e1; e += kU * 256) {
+          for (int e = e0 + t; e < e1; e += kU * CONS) {
             uint32_t w[kU];
             int bk[kU];
             double v[kU], acc[kU];
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
-              const int eu = e + u * 256;
+              const int eu = e + u * CONS;
               w[u] = eu < e1 ? slst[eu] : kPadWord;
               bk[u] = (int)((w[u] >> kLE) & ((1u << kBucketBits) - 1)) - a.b0;
             }
@@ -551,15 +558,15 @@ __global__ void __launch_bounds__(512, 1) cm_pass2_ws_kernel(const PassArgs a) {
             if ((unsigned)bk < (unsigned)a.nb) sa[bk] = (w >> 31) ? sa[bk] - tile[w & (kE - 1)] : sa[bk] + tile[w & (kE - 1)];
           }
         }
-        nbar_sync(kBarCons, 256);
+        nbar_sync(kBarCons, CONS);
       }
-      if (i + 2 < nitems) nbar_arrive(kBarEmpty + b, 512);  // buffer b free (no arrival left unmatched)
+      if (i + 2 < nitems) nbar_arrive(kBarEmpty + b, NALL);  // buffer b free (no arrival left unmatched)
       if (tt == a.ntiles - 1) {  // column done: SA column out (the last round ended with a consumer barrier)
         if (col < a.ncols) {
           double* o = col < a.ncolSA ? a.SA + col * a.ldsa : a.Sb;
-          for (int k = t; k < a.nb; k += 256) o[a.b0 + k] = a.alpha * sa[k];
+          for (int k = t; k < a.nb; k += CONS) o[a.b0 + k] = a.alpha * sa[k];
         }
-        nbar_sync(kBarCons, 256);  // sa is zeroed for the next column
+        nbar_sync(kBarCons, CONS);  // sa is zeroed for the next column
       }
     }
   }
@@ -851,12 +858,13 @@ bool use_ws(int K2, int s) {
 template <int K2>
 int launch_pass2_ws(const PassArgs& a, cudaStream_t st) {
   const size_t smem = ws_smem_bytes(a.s, a.nb);
-  auto* f = cm_pass2_ws_kernel<K2>;
+  constexpr int CONS = SKH_WS_CONS;
+  auto* f = cm_pass2_ws_kernel<K2, CONS>;
   int rc = set_smem(f, smem);
   if (rc) return rc;
   const int64_t grid = std::min<int64_t>(a.ncols, (int64_t)num_sms());
   if (grid < 1) return SKH_OK;
-  f<<<(unsigned)grid, 512, smem, st>>>(a);
+  f<<<(unsigned)grid, 256 + CONS, smem, st>>>(a);
   note_launch();
   return check_launch("cm_pass2_ws");
 }
