@@ -1,0 +1,92 @@
+"""Host logic of bench.py (no GPU): the roofline object for every path and the
+reference arm's JSON line (the CPU oracle on a bounded sample)."""
+import importlib.util
+import json
+import os
+import subprocess
+import sys
+import types
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def bench():
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def cfg_of(name):
+    sys.path.insert(0, ROOT)
+    from synth import configs
+    return configs.ALL[name]
+
+
+PEAK = 6552.6
+
+
+def check(r, alg, ms):
+    assert r["unit"] == "GB/s" and r["bound"] == "hbm" and r["peak"] == PEAK
+    assert r["alg_bytes_per_launch"] == alg
+    assert abs(r["achieved"] - alg / (ms / 1e3) / 1e9) <= 0.1
+    assert abs(r["frac"] - r["achieved"] / PEAK) <= 1e-3
+
+
+def test_roofline_fwht_uses_mean_pass_time_and_plan():
+    b, cfg = bench(), cfg_of("C5")
+    step = types.SimpleNamespace(plan=[7, 7, 7], n_pad=cfg.n)
+    st = {"hash_gen": 0.1, "fwht_pass0": 20.0, "fwht_pass1": 21.0, "fwht_pass2": 22.0, "gather": 9.7}
+    r = b.roofline(cfg, step, st, PEAK, "test")
+    check(r, 2 * cfg.n * cfg.d * 8, 21.0)
+    assert "7+7+7" in r["kernel"]
+
+
+def test_roofline_gather_csr_and_dht():
+    b = bench()
+    c3 = cfg_of("C3")
+    r = b.roofline(c3, None, {"hash_gen": 0.06, "gather": 0.95}, PEAK, "test")
+    check(r, c3.n * c3.d * 8 + c3.m * c3.d * 8 + c3.n * c3.s * 5, 0.95)
+    assert r["kernel"] == "gather_wide"
+    c4 = cfg_of("C4")
+    r = b.roofline(c4, None, {"hash_gen": 0.14, "gather_csr": 0.57}, PEAK, "test")
+    check(r, c4.n * c4.nnz_row * 12 + (c4.n + 1) * 8 + c4.m * c4.d * 8 + c4.n * c4.s * 5, 0.57)
+    c2 = cfg_of("C2")
+    st = {"hash_gen": 0.03, "dht_passA": 0.25, "dht_passB": 0.20, "gather": 0.11}
+    r = b.roofline(c2, None, st, PEAK, "test", sketch="dht")
+    check(r, 2 * c2.n * (c2.d + 1) * 8, 0.25)
+    assert r["kernel"] == "dht_passA"
+
+
+def test_roofline_column_major_paths():
+    b = bench()
+    c5 = cfg_of("C5")
+    step = types.SimpleNamespace(n_pad=c5.n)
+    st = {"hash_gen": 0.1, "tile_lists": 0.2, "pass1": 24.0, "pass2_gather": 38.5}
+    r = b.roofline(c5, step, st, PEAK, "test", layout="col")
+    cols = c5.d + 1
+    check(r, c5.n * cols * 8 + c5.m * cols * 8 + c5.n * c5.s * 4, 38.5)
+    assert r["kernel"] == "cm_pass2_gather"
+    c3 = cfg_of("C3")
+    st = {"hash_gen": 0.06, "transpose": 1.55, "gather": 1.05}
+    r = b.roofline(c3, types.SimpleNamespace(n_pad=c3.n), st, PEAK, "test", layout="col")
+    check(r, 2 * c3.n * c3.d * 8, 1.55)
+    assert "transpose" in r["kernel"]
+
+
+@pytest.mark.timeout(600)
+def test_reference_arm_json_line():
+    """`bench.py --impl reference` (the CPU oracle) prints one JSON line with the
+    contract's keys, on the C1 workload, without a GPU."""
+    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
+                        "--workload", "C1"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0 and line["config"]["workload"] == "C1"
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["value"] == line["value"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
