@@ -261,7 +261,22 @@ def test_determinism_stress_shared_memory_paths():
     rp, ci, v = (torch.from_numpy(x).cuda() for x in gen.csr(c4))
     bl = skh().hash_gen(c4.seed, c4.m, c4.s, c4.n)
     runs3 = [skh().sketch_csr(bl, rp, ci, v, c4.d) for _ in range(5)]
-    for rr in (runs, runs2, runs3):
+    # the count-based CSR reduce (every bucket's run fits in registers)
+    bl2 = skh().hash_gen(c4.seed, 2000, c4.s, c4.n)
+    runs4 = [skh().sketch_csr(bl2, rp, ci, v, c4.d) for _ in range(5)]
+    # the on-chip walk of the plain column-major sketch (small workspace)
+    runs5 = [skh().sketch_dense_colmajor(cfg.seed, At, b, cfg.m, 3, fast=False) for _ in range(5)]
+    # K2 = 8 (two-CTA pass 2) and K2 = 4 (warp-specialised) column-major transforms
+    c8 = configs.C5.scaled(n=1 << 21, d=2, m=700)
+    At8 = device.dense_colmajor(c8)
+    runs6 = [skh().rht_dense_colmajor(c8.seed, At8, None, c8.m, 1) for _ in range(5)]
+    c4b = configs.C5.scaled(n=1 << 17, d=5, m=700)
+    At4 = device.dense_colmajor(c4b)
+    runs7 = [skh().rht_dense_colmajor(c4b.seed, At4, None, c4b.m, 2) for _ in range(5)]
+    # the HR-DHT passes (shared-memory FFT rounds)
+    A2 = device.dense(configs.C2.scaled(n=1 << 14, d=40, m=100))
+    runs8 = [skh().hrdht_dense(3, A2, None, 100, 2) for _ in range(5)]
+    for rr in (runs, runs2, runs3, runs4, runs5, runs6, runs7, runs8):
         for SA, Sb in rr[1:]:
             assert torch.equal(SA, rr[0][0])
             if Sb is not None:
