@@ -109,11 +109,21 @@ def oracle_sample(cfg, ncols):
 
 
 def cpu_baseline(cfg, target_s=12.0):
+    """The oracle on a bounded column sample sized to ~target_s seconds: the
+    per-sample fixed cost (drawing S for all n rows) is separated from the
+    per-column cost with two probes, then the column count is chosen."""
     ncols = 1
     nbytes, t, what = oracle_sample(cfg, ncols)
     if t < target_s / 2 and cfg.kind != "csr":
-        ncols = max(1, min(cfg.d, int(ncols * target_s / max(t, 1e-3))))
-        nbytes, t, what = oracle_sample(cfg, ncols)
+        n2 = max(2, min(cfg.d, 4))
+        nb2, t2, what2 = oracle_sample(cfg, n2)
+        per_col = max((t2 - t) / (n2 - 1), 1e-4)
+        fixed = max(t - per_col, 0.0)
+        ncols = max(n2, min(cfg.d, int((target_s - fixed) / per_col)))
+        if ncols > n2 and t2 < target_s / 2:
+            nbytes, t, what = oracle_sample(cfg, ncols)
+        else:
+            nbytes, t, what = nb2, t2, what2
     return {"value": nbytes / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
             "sample": f"{what}; {t:.2f} s single-threaded NumPy", "seconds": round(t, 3)}
 
