@@ -235,6 +235,17 @@ int skh_sketch_dense_host(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_
 int skh_scale(double* X, int64_t rows, int64_t cols, int64_t ldx, double alpha,
               void* stream);
 
+/* Exchange-free sharded H D A: with
+ * H_n = H_G (x) H_L (L = n / G, row i = g L + l), rank r's contribution is
+ * T_r Z_r with Z_r = H_L D A_r (its local rows, all local stages) and
+ * T_r = sum_g (-1)^popcount(g & r) S_g (S_g: columns g L .. g L + L - 1 of S).
+ * Given bucket lists of all n columns of S (skh_hash_gen, row0 = 0, nrows =
+ * n, rows = global j), this rewrites them in place into T_r's lists: row
+ * j -> j mod L, sign times (-1)^popcount((j / L) & r).  Entries keep their
+ * ascending-j order (a fixed summation order). */
+int skh_fold_lists(int64_t nentries, int32_t* bucket_rows, int8_t* bucket_signs,
+                   int64_t L, int64_t rank, void* stream);
+
 /* Deterministic ordered sum of G partial blocks laid out consecutively:
  * out[r, c] = (((P_0[r,c] + P_1[r,c]) + P_2[r,c]) + ...) * alpha, where
  * P_g = parts + g * part_stride (elements), each [rows x cols] with ld `ldp`.

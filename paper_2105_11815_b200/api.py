@@ -259,6 +259,18 @@ def scale(X, alpha):
     return X
 
 
+def fold_lists(bl, L, rank):
+    """In place: bucket lists of all n columns of S (global rows) -> the lists of
+    T_rank = sum_g (-1)^popcount(g & rank) S_g over local rows j mod L
+    (skh_fold_lists; the exchange-free sharded H D A)."""
+    lib = _lib.load()
+    _need_cuda(bl.rows)
+    _lib.check(lib.skh_fold_lists(bl.rows.numel(), _ptr(bl.rows), _ptr(bl.signs), int(L), int(rank), _stream()),
+               "skh_fold_lists")
+    bl.nrows = int(L)
+    return bl
+
+
 def ordered_sum(parts, alpha=1.0, out=None):
     """parts: [G, rows, cols] contiguous; out = alpha * (((P0 + P1) + P2) + ...)."""
     lib = _lib.load()

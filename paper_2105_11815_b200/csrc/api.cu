@@ -55,6 +55,17 @@ __global__ void scale_kernel(double* X, int64_t rows, int64_t cols, int64_t ldx,
   X[r * ldx + c] = alpha * X[r * ldx + c];
 }
 
+// M3 fold (exchange-free sharded H D A): global column j of S
+// -> local row j mod L, sign times (-1)^popcount((j / L) & rank)
+__global__ void fold_lists_kernel(int64_t N, int32_t* __restrict__ rows, int8_t* __restrict__ signs, int64_t L,
+                                  int64_t rank) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N) return;
+  const int64_t j = rows[e];
+  rows[e] = (int32_t)(j % L);
+  if (__popcll((unsigned long long)((j / L) & rank)) & 1) signs[e] = (int8_t)(-signs[e]);
+}
+
 __global__ void ordered_sum_kernel(const double* __restrict__ P, int64_t G, int64_t pstride, int64_t rows,
                                    int64_t cols, int64_t ldp, double* __restrict__ out, int64_t ldo, double alpha) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -603,6 +614,19 @@ int skh_scale(double* X, int64_t rows, int64_t cols, int64_t ldx, double alpha, 
   if (N == 0) return SKH_OK;
   scale_kernel<<<(unsigned)((N + 255) / 256), 256, 0, as_stream(stream)>>>(X, rows, cols, ldx, alpha); note_launch();
   return check_launch("scale");
+}
+
+int skh_fold_lists(int64_t nentries, int32_t* bucket_rows, int8_t* bucket_signs, int64_t L, int64_t rank,
+                   void* stream) {
+  if (nentries < 0 || L < 1 || rank < 0 || (nentries > 0 && (!bucket_rows || !bucket_signs))) {
+    set_error("fold_lists: invalid arguments");
+    return SKH_EINVAL;
+  }
+  if (nentries == 0) return SKH_OK;
+  fold_lists_kernel<<<(unsigned)((nentries + 255) / 256), 256, 0, as_stream(stream)>>>(nentries, bucket_rows,
+                                                                                      bucket_signs, L, rank);
+  note_launch();
+  return check_launch("fold_lists");
 }
 
 int skh_ordered_sum(const double* parts, int64_t G, int64_t part_stride, int64_t rows, int64_t cols, int64_t ldp,

@@ -43,6 +43,9 @@ class CudaOps:
     def ordered_sum(self, parts, alpha, out=None):
         return self.api.ordered_sum(parts, alpha=alpha, out=out)
 
+    def fold_lists(self, bl, L, rank):
+        return self.api.fold_lists(bl, L, rank)
+
     def c_ns(self, n_pad, s):
         return self.api.c_ns(n_pad, s)
 
@@ -196,6 +199,86 @@ class ShardedHrht:
         finish(self.K - 1)
         mark("pipeline")
         # R6 (M5): strips to their owners, then a rank-order sum scaled once by c_ns
+        lo, hi = self.strips[r]
+        if G > 1:
+            all_to_all(self.R.view(G * self.mq, self.d), self.P, group=self.group)
+            if self.b is not None:
+                all_to_all(self.Rb.view(-1), self.Pb, group=self.group)
+        else:
+            self.R[0].copy_(self.P)
+            if self.b is not None:
+                self.Rb[0].copy_(self.Pb)
+        ops.ordered_sum(self.R, self.alpha, out=self.out)
+        Sb = None
+        if self.b is not None:
+            ops.ordered_sum(self.Rb.view(G, self.mq, 1), self.alpha, out=self.outb)
+            Sb = self.outb[: hi - lo, 0]
+        mark("reduce")
+        return self.out[: hi - lo], Sb, (lo, hi)
+
+
+class ShardedHrhtM3:
+    """SA = S_h H D A over G ranks WITHOUT the butterfly all-to-all (SURVEY §8(e)
+    M3): H_n = H_G (x) H_L (L = n / G), so with Z_r = H_L D A_r (the local rows,
+    every local stage, D with global ids)
+
+        S H D A = sum_r T_r Z_r,   T_r = sum_g (-1)^popcount(g & r) S_g,
+
+    S_g the columns g L .. g L + L - 1 of S.  Each rank draws S for all n
+    columns (cheap: n s entries), folds the lists into T_r's (skh_fold_lists:
+    row j -> j mod L, sign times (-1)^popcount((j / L) & r)), gathers its local
+    Z_r with them (every local row is read by G s list entries) and the partials
+    meet in the same deterministic strip reduction as ShardedHrht (R6).  The only
+    collective is that reduction: |SA| per rank instead of the (G-1)/G |A_r|
+    all-to-all.  Rounding differs from the single-GPU order (the H_G butterflies
+    are folded into the sums): 1e-12, bit-identical on integer inputs."""
+
+    STAGES = ("hash_gen", "transform", "gather", "reduce")
+
+    def __init__(self, seed, A_loc, b_loc, n, m, s, ops=None, group=None):
+        self.ops = ops or CudaOps()
+        self.group = group
+        self.G = dist.get_world_size(group)
+        self.r = dist.get_rank(group)
+        self.seed, self.n, self.m, self.s = seed, int(n), int(m), int(s)
+        self.L = self.n // self.G
+        if self.L * self.G != self.n or A_loc.shape[0] != self.L:
+            raise ValueError("A_loc must hold n / G rows")
+        _log2(self.n)
+        self.lg = _log2(self.L)
+        self.A, self.b = A_loc, b_loc
+        d = A_loc.shape[1]
+        self.d = d
+        kw = dict(dtype=A_loc.dtype, device=A_loc.device)
+        self.Z = torch.empty(self.L, d, **kw)
+        self.zb = torch.empty(self.L, 1, **kw) if b_loc is not None else None
+        self.mq, self.strips = strip_rows(self.m, self.G)
+        self.P = torch.zeros(self.G * self.mq, d, **kw)
+        self.Pb = torch.zeros(self.G * self.mq, **kw) if b_loc is not None else None
+        self.R = torch.empty(self.G, self.mq, d, **kw)
+        self.Rb = torch.empty(self.G, self.mq, **kw) if b_loc is not None else None
+        self.out = torch.empty(self.mq, d, **kw)
+        self.outb = torch.empty(self.mq, 1, **kw) if b_loc is not None else None
+        self.bl = None
+        self.alpha = self.ops.c_ns(self.n, self.s)
+        self.ws = None
+        if isinstance(self.ops, CudaOps):
+            self.ws = self.ops.api.rht_stages_workspace(self.L, self.L, self.r * self.L, d, A_loc.device)
+
+    def run(self, mark=None):
+        mark = mark or (lambda name: None)
+        ops, G, r, L = self.ops, self.G, self.r, self.L
+        # S for all n columns (global row ids), folded into T_r over local rows
+        self.bl = ops.hash_gen(self.seed, self.m, self.s, self.n, 0, 0, 0, out=self.bl)
+        ops.fold_lists(self.bl, L, r)
+        mark("hash_gen")
+        ops.rht_stages(self.seed, self.A, 0, self.lg, L, r * L, True, self.Z, self.ws)
+        if self.b is not None:
+            ops.rht_stages(self.seed, self.b.view(-1, 1), 0, self.lg, L, r * L, True, self.zb, self.ws)
+        mark("transform")
+        ops.sketch_dense(self.bl, self.Z, None if self.b is None else self.zb.view(-1), 1.0, SA=self.P[: self.m],
+                         Sb=None if self.b is None else self.Pb[: self.m])
+        mark("gather")
         lo, hi = self.strips[r]
         if G > 1:
             all_to_all(self.R.view(G * self.mq, self.d), self.P, group=self.group)

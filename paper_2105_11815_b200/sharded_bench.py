@@ -64,7 +64,11 @@ def run(args, cfg):
         L = cfg.n // G
         A = device.dense(cfg, rank * L, (rank + 1) * L)
         b = device.rhs(cfg, rank * L, (rank + 1) * L)
-        step = sharded.ShardedHrht(cfg.seed, A, b, cfg.n, cfg.m, cfg.s)
+        # SKH_SHARDED_HD=m3: the exchange-free variant (H_G folded into the sketch)
+        if os.environ.get("SKH_SHARDED_HD", "m2") == "m3":
+            step = sharded.ShardedHrhtM3(cfg.seed, A, b, cfg.n, cfg.m, cfg.s)
+        else:
+            step = sharded.ShardedHrht(cfg.seed, A, b, cfg.n, cfg.m, cfg.s)
         shard = (A, b)
     else:
         per = (cfg.n + G - 1) // G
@@ -154,7 +158,22 @@ def run(args, cfg):
                            "note": cfg.note},
                 "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
                 "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e}
-        if cfg.hd:
+        if cfg.hd and isinstance(step, sharded.ShardedHrhtM3):
+            # per rank: the local FWHT passes over L rows, then a gather whose lists
+            # read every local row G s times (the folded H_G)
+            L = cfg.n // G
+            npass = len(api.rht_pass_plan((L).bit_length() - 1, cfg.d))
+            t = stage_ms["transform"]
+            alg = npass * 2 * L * cfg.d * 8
+            ach = alg / (t / 1e3) / 1e9
+            line["roofline"] = {"bound": "hbm", "kernel": f"local FWHT passes per rank ({npass})",
+                                "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                                "frac": round(ach / pk["hbm_gbs"], 4), "traffic": None, "peak_source": src,
+                                "gather_ms": round(stage_ms["gather"], 4),
+                                "gather_row_reads_per_local_row": G * cfg.s}
+            line["comm"] = {"all_to_all_rows_bytes_sent_per_rank": 0,
+                            "strip_reduction_bytes_per_rank": (G - 1) * ((cfg.m + G - 1) // G) * cfg.d * 8}
+        elif cfg.hd:
             # the column-chunk pipeline interleaves the kernels with the (overlapped)
             # all-to-all, so the roofline is taken over the whole pipeline stage:
             # algorithmic HBM bytes of the local passes, the cross-stage pass and

@@ -47,6 +47,14 @@ def _worker(rank, G, port, kind, out_dir):
             ok &= np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
             if kind == "int":
                 ok &= np.array_equal(got, ref)
+        m3 = sharded.ShardedHrhtM3(seed, At, bt, n, m, s)  # exchange-free: skh_fold_lists + one gather
+        strip, sb, lohi = m3.run()
+        SA = sharded.gather_strips(strip, lohi, m).cpu().numpy()
+        Sb = sharded.gather_strips(sb, lohi, m).cpu().numpy()
+        for got, ref in ((SA, want), (Sb, wantb)):
+            ok &= np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
+            if kind == "int":
+                ok &= np.array_equal(got, ref)
         pl = sharded.ShardedPlain(seed, At, bt, n, m, 2)
         strip, sb, lohi = pl.run()
         SA = sharded.gather_strips(strip, lohi, m).cpu().numpy()

@@ -56,6 +56,13 @@ class OracleOps:
         out.copy_(alpha * acc)
         return out
 
+    def fold_lists(self, bl, L, rank):
+        j = np.asarray(bl.rows, dtype=np.int64)
+        par = np.array([bin(int(g) & rank).count("1") & 1 for g in (j // L)], dtype=np.int64)
+        bl.rows = (j % L).astype(bl.rows.dtype)
+        bl.signs = np.where(par == 1, -np.asarray(bl.signs), np.asarray(bl.signs)).astype(np.asarray(bl.signs).dtype)
+        return bl
+
     def c_ns(self, n_pad, s):
         return sketch.c_ns(n_pad, s)
 
@@ -90,6 +97,15 @@ def _worker(rank, G, port, case):
         SA = sharded.gather_strips(strip, (lo, hi), m).numpy()
         Sb = sharded.gather_strips(sb, (lo, hi), m).numpy()
         want, wantb = sketch.rht_sketch(seed, A, b, m, s)
+        for got, ref in ((SA, want), (Sb, wantb)):
+            assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
+            if kind == "int":
+                assert np.array_equal(got, ref)
+        # the exchange-free variant (M3): H_G folded into the sketch
+        m3 = sharded.ShardedHrhtM3(seed, At, bt, n, m, s, ops=ops)
+        strip, sb, (lo, hi) = m3.run()
+        SA = sharded.gather_strips(strip, (lo, hi), m).numpy()
+        Sb = sharded.gather_strips(sb, (lo, hi), m).numpy()
         for got, ref in ((SA, want), (Sb, wantb)):
             assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
             if kind == "int":
