@@ -253,3 +253,20 @@ print(json.dumps({"x": x.cpu().numpy().tolist(), "info": info}))
     assert all(o["info"]["step"] == 4 for o in outs)
     assert abs(outs[0]["info"]["iters"] - outs[1]["info"]["iters"]) <= 2
     assert max(r) <= best * (1 + 1e-10)
+
+
+def test_lls_colmajor_tall_two_row_product():
+    """Column-major A with n >= 2^19 takes cm_av2_kernel (two rows per thread,
+    16-byte column segments; odd n leaves one row for the tail path): the solve
+    reaches the least-squares minimiser like the row-major path."""
+    from oracle import sketch
+    n, d, m = (1 << 19) + 1, 6, 60
+    A, b = ill_conditioned(n, d, 7, 1e3)
+    SA, Sb = sketch.sketch_dense(3, A, b, m, 2)
+    solver = skh().LlsSolver(n, d, m)
+    x, info = solver(torch.from_numpy(np.ascontiguousarray(A.T)).cuda(), torch.from_numpy(b).cuda(),
+                     torch.from_numpy(np.ascontiguousarray(SA.T)).cuda(), torch.from_numpy(Sb).cuda(), colmajor=True)
+    xs = np.linalg.lstsq(A, b, rcond=None)[0]
+    best = np.linalg.norm(A @ xs - b)
+    assert info["step"] in (3, 4)
+    assert np.linalg.norm(A @ np_(x) - b) <= best * (1 + 1e-10)
