@@ -119,7 +119,8 @@ def cpu_baseline(cfg, target_s=12.0):
         nb2, t2, what2 = oracle_sample(cfg, n2)
         per_col = max((t2 - t) / (n2 - 1), 1e-4)
         fixed = max(t - per_col, 0.0)
-        cap = max(n2, (256 << 20) // (cfg.n * 8))  # host memory: <= 256 MB of A per sample
+        # host memory per sample: <= 512 MB of A under H D (its transform's temporaries), 1 GB plain
+        cap = max(n2, ((512 << 20) if cfg.hd else (1 << 30)) // (cfg.n * 8))
         ncols = max(n2, min(cfg.d, cap, int((target_s - fixed) / per_col)))
         if ncols > n2 and t2 < target_s / 2:
             nbytes, t, what = oracle_sample(cfg, ncols)

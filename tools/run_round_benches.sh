@@ -10,3 +10,4 @@ mkdir -p gpurun_out/sketches
 for w in C2 C3HD; do for sk in dht srdht; do python bench.py --workload $w --sketch $sk --steps 10 --no-alt-layout > gpurun_out/sketches/bench_${w}_${sk}.log 2>&1; done; done
 for w in C2 C3 C3HD C4 C5; do python bench.py --workload $w --sketch variant --steps 10 --no-alt-layout > gpurun_out/sketches/bench_${w}_variant.log 2>&1; done
 for w in C2 C3HD; do SKH_LLS_RINV=1 timeout 300 python tools/bench_lls.py $w 2 >> gpurun_out/final/lls_bench.log 2>&1; done
+for w in C2 C5; do timeout 300 python tools/bench_lls.py $w 2 col >> gpurun_out/final/lls_bench.log 2>&1; done
