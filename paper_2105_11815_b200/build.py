@@ -5,6 +5,7 @@
 
 Usage: python -m paper_2105_11815_b200.build [--force]
 """
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -41,7 +42,19 @@ def _stale(out, srcs):
     return any(os.path.getmtime(s) > t for s in _deps(srcs) if os.path.exists(s))
 
 
+def _compile(src, obj, verbose):
+    cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc failed on {src}")
+    if verbose:
+        sys.stderr.write(r.stderr)
+    return obj
+
+
 def build(force=False, verbose=False):
+    """Compile stale objects (in parallel) and relink stale libraries."""
     built = []
     for out, srcs in TARGETS.items():
         if not srcs:
@@ -50,17 +63,11 @@ def build(force=False, verbose=False):
             continue
         objdir = os.path.join(os.path.dirname(out), "build_obj")
         os.makedirs(objdir, exist_ok=True)
-        objs = []
-        for s in srcs:
-            o = os.path.join(objdir, os.path.basename(s).replace(".cu", ".o"))
-            cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if r.returncode != 0:
-                sys.stderr.write(r.stdout + r.stderr)
-                raise RuntimeError(f"nvcc failed on {s}")
-            if verbose:
-                sys.stderr.write(r.stderr)
-            objs.append(o)
+        objs = [os.path.join(objdir, os.path.basename(s).replace(".cu", ".o")) for s in srcs]
+        todo = [(s, o) for s, o in zip(srcs, objs) if force or _stale(o, [s])]
+        with concurrent.futures.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+            for f in [ex.submit(_compile, s, o, verbose) for s, o in todo]:
+                f.result()
         cmd = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart", *LIBS.get(out, [])]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

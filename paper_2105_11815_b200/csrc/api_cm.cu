@@ -16,7 +16,7 @@ int cm_max_buckets(int s);
 int launch_cm_pass1(uint64_t seed, const double* X, int64_t ldx, int64_t ncolX, const double* xb, double* Y,
                     int64_t ldy, int64_t nvalid, int L, int apply_diag, int64_t row0, cudaStream_t st);
 int launch_cm_mid(double* Y, int64_t ldy, int64_t ncols, int64_t nrows, int lo, int K2, cudaStream_t st);
-size_t cm_lists_bytes(int64_t ntiles, int s);
+size_t cm_lists_bytes(int64_t ntiles, int s, int64_t m);
 int launch_cm_lists(const int32_t* col_rows, const int8_t* col_signs, int s, int64_t m, int K2, int lo,
                     int64_t nvalid, int64_t ntiles, void* lists_ws, cudaStream_t st);
 int launch_cm_gather(const double* X, int64_t ldx, int64_t ncolX, const double* xb, int64_t nvalid, int64_t ntiles,
@@ -27,7 +27,6 @@ namespace {
 
 constexpr int kCmP1 = 13;     // bits of pass 1
 constexpr int kCmTile = 12;   // log2 positions of a pass-2 tile
-constexpr int64_t kCmMaxM = 65536;
 
 // ---- stage trace (thread-local)
 struct Trace {
@@ -89,10 +88,6 @@ int validate(int64_t n, int64_t m, int32_t s, int64_t d, int64_t nrows_hash) {
               (long long)m, s, (long long)d);
     return SKH_EINVAL;
   }
-  if (m > kCmMaxM) {
-    set_error("colmajor: m = %lld exceeds %lld (on-chip rank counters)", (long long)m, (long long)kCmMaxM);
-    return SKH_EINVAL;
-  }
   if (nrows_hash * (int64_t)s >= (1ll << 31)) {
     set_error("colmajor: n*s exceeds int32 indices");
     return SKH_EOVERFLOW;
@@ -133,7 +128,7 @@ CmWs cm_layout(void* base, int64_t nrows_hash, int64_t ycols, int64_t yrows, int
   w.rows = (int32_t*)take(sizeof(int32_t) * (size_t)nrows_hash * s);
   w.signs = (int8_t*)take((size_t)nrows_hash * s);
   w.hws = take(hash_ws_bytes(nrows_hash, m, s));
-  w.lists = take(cm_lists_bytes(ntiles, s));
+  w.lists = take(cm_lists_bytes(ntiles, s, m));
   w.total = off;
   return w;
 }

@@ -14,10 +14,10 @@
 // three-pass plan.
 //
 // Determinism without atomics: the rows of a pass-2 tile are the same for every
-// column, so its (position p, draw q) entries are sorted once per sketch by
-// rank -- the number of earlier positions of the tile hashed to the same bucket
-// -- into a tile list (cm_lists_kernel).  Pass 2 adds every rank-0 entry (all in
-// distinct buckets), syncs, then rank 1, and so on: a bucket receives a tile's
+// column, so a plan built once per sketch (cm_plan_kernel) gives each bucket
+// the tile hits to exactly ONE consumer thread, with all of that bucket's
+// entries of the tile in ascending row order; threads add only into their own
+// buckets and tiles are separated by one barrier.  A bucket receives a tile's
 // entries in ascending row order and the tiles in order.  That order is fixed
 // (bitwise reproducible), but for the transform path it is not the oracle's
 // ascending order across the whole bucket (R17): SA agrees with the
@@ -41,13 +41,6 @@ namespace {
 constexpr int kP1Bits = 13;            // pass-1 tile: 2^13 contiguous rows (64 KiB)
 constexpr int kLE = 12;                // pass-2 tile: 4096 positions per column
 constexpr int kE = 1 << kLE;
-constexpr int kRounds = 32;            // rank rounds per tile; the last one is serial
-constexpr int kBucketBits = 19;        // list word: p (12) | bucket (19) | sign (1)
-constexpr uint32_t kPadWord = 0xFFFFFFFFu;  // empty slot (bucket field >= any m)
-constexpr int kRoffStride = 36;             // round offsets per tile (33 used; 144 B, 16-byte aligned)
-
-// Words of one tile list: E s entries + 25 % for the bank-class padding.
-__host__ __device__ constexpr int list_cap(int s) { return kE * s + (kE * s) / 4; }
 
 // ------------------------------------------------------------------ pass 1
 // 16-byte slot swizzle: conflict-free for the three layouts below.
@@ -271,10 +264,10 @@ struct PassArgs {
   int64_t nvalid;  // rows >= nvalid read as zero
   int64_t ntiles;  // tiles per column
   int lo;
-  double* Y;       // !GATHER: output column c at Y + c ldy
+  double* Y;       // mid passes: output column c at Y + c ldy
   int64_t ldy;
-  const uint32_t* lists;  // GATHER: [ntiles][4096 s] rank-sorted tile entries
-  const int32_t* roff;    // [ntiles][kRounds + 1] round offsets
+  const uint32_t* words;  // gather: [ntiles][plan_jcap(s)][kNC] owner plan words
+  const int32_t* hdr;     // gather: [ntiles] steps J of the tile (< 0: serial list of -J words)
   int s;
   int b0, nb;             // buckets [b0, b0 + nb) accumulated by this launch
   double* SA;             // output column c < ncolSA at SA + c ldsa, column ncolSA at Sb
@@ -287,289 +280,394 @@ template <int K2>
 __device__ __forceinline__ void load_tile(const PassArgs& a, int64_t col, int64_t tt, int t, double (&x)[16]) {
   const double* src = col < a.ncols ? col_in(a.X, a.ldx, a.ncolX, a.xb, col) : nullptr;
   const int64_t rb = tile_row(tt, Geo<K2>::p0(t, 0), K2, a.lo);
+  // rows of this thread's values: rb + vk 2^lo + WT u -- one base pointer and
+  // compile-time multiples of the two strides; the bounds test is per tile
+  const int64_t last = rb + ((int64_t)(16 / Geo<K2>::VJ - 1) << a.lo) + (int64_t)Geo<K2>::WT * (Geo<K2>::VJ - 1);
+  if (src && last < a.nvalid) {
+    const double* p = src + rb;
+    const int64_t sk = (int64_t)1 << a.lo;
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = __ldg(p + (v / Geo<K2>::VJ) * sk + Geo<K2>::WT * (v % Geo<K2>::VJ));
+    return;
+  }
 #pragma unroll
   for (int v = 0; v < 16; ++v) {
-    // rows of this thread's values: rb + (k - k0) 2^lo + WT u, one base + strides
     const int vk = v / Geo<K2>::VJ, u = v % Geo<K2>::VJ;
     const int64_t r = rb + ((int64_t)vk << a.lo) + (int64_t)Geo<K2>::WT * u;
     x[v] = (src && r < a.nvalid) ? __ldg(src + r) : 0.0;
   }
 }
 
-// Value type of NC columns at one position.
-template <int NC> struct Vec;
-template <> struct Vec<1> {
-  using T = double;
-  __device__ static __forceinline__ T zero() { return 0.0; }
-  __device__ static __forceinline__ T addsub(T acc, T v, bool neg) { return neg ? acc - v : acc + v; }
-  __device__ static __forceinline__ double get(T v, int) { return v; }
-};
-
-// Persistent: CTA works on column groups (NC = 1 column) blockIdx.x,
-// + gridDim.x, ...; for each, the ntiles tiles in order.  The next work item's
-// 16 values per thread are loaded into registers while the current one is
-// transformed and gathered.  256 threads per column.  Measured on B200 (C5):
-// bound by shared-memory traffic and barrier latency of the rank-round scatter
-// (~0.5 wavefronts per element against an HBM budget of ~0.3 cycles per
-// element), not by HBM; a cp.async ring (3 tiles in flight) and two columns
-// per CTA were both slower.
-template <int K2, bool GATHER, int NC>
-__global__ void __launch_bounds__(256 * NC, 2 / NC) cm_pass2_kernel(const PassArgs a) {
-  using V = typename Vec<NC>::T;
-  constexpr int NT = 256 * NC;
+// Mid pass (no gather): bits [lo, lo + K2) of 4096-position tiles, in place.
+// Persistent CTA over (column, tile) items; the next item's 16 values per
+// thread are loaded while the current one is transformed.
+template <int K2>
+__global__ void __launch_bounds__(256, 2) cm_mid_kernel(const PassArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  // [0, NC*32K): exchange buffer (NC x 4096 doubles) / final tile (4096 x NC doubles)
-  constexpr int kTileBytes = NC * kE * 8;
-  double* ex = reinterpret_cast<double*>(smraw);
-  V* tile = reinterpret_cast<V*>(smraw);
-  int32_t* sroff = reinterpret_cast<int32_t*>(smraw + kTileBytes);                   // [kRounds + 1] (+pad)
-  uint32_t* slst = reinterpret_cast<uint32_t*>(smraw + kTileBytes + 256);            // [list_cap(s)]
-  V* sa = reinterpret_cast<V*>(smraw + kTileBytes + 256 + (size_t)4 * list_cap(a.s));  // [nb]
-
-  const int tid = threadIdx.x, h = tid >> 8, t = tid & 255;
-  const int64_t ngroups = (a.ncols + NC - 1) / NC;
-  const int64_t my_groups = ngroups > blockIdx.x ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t nitems = my_groups * a.ntiles;
-  const int nlw = GATHER ? list_cap(a.s) / 4 : 0;  // 16-byte chunks of one tile list
-
-  auto group_of = [&](int64_t i) { return (int64_t)blockIdx.x + (i / a.ntiles) * gridDim.x; };
-  auto issue_list = [&](int64_t tt) {
-    if (!GATHER) return;
-    const uint4* gl = reinterpret_cast<const uint4*>(a.lists + tt * (int64_t)list_cap(a.s));
-    for (int i = tid; i < nlw; i += NT) {
-      const unsigned dsts = (unsigned)__cvta_generic_to_shared(slst + 4 * i);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dsts), "l"(gl + i));
-    }
-    if (tid < kRounds + 1) sroff[tid] = a.roff[tt * kRoffStride + tid];
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
-
+  double* ex = reinterpret_cast<double*>(smraw);  // [4096] exchange buffer
+  const int t = threadIdx.x;
+  const int64_t my_cols = a.ncols > blockIdx.x ? (a.ncols - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t nitems = my_cols * a.ntiles;
+  auto col_of = [&](int64_t i) { return (int64_t)blockIdx.x + (i / a.ntiles) * gridDim.x; };
   double x[16], xn[16];
-  if (nitems > 0) {
-    load_tile<K2>(a, NC * group_of(0) + h, 0, t, xn);
-    issue_list(0);
-  }
+  if (nitems > 0) load_tile<K2>(a, col_of(0), 0, t, xn);
   for (int64_t i = 0; i < nitems; ++i) {
-    const int64_t grp = group_of(i), tt = i % a.ntiles;
+    const int64_t tt = i % a.ntiles, col = col_of(i);
 #pragma unroll
     for (int v = 0; v < 16; ++v) x[v] = xn[v];
-    if (i + 1 < nitems) load_tile<K2>(a, NC * group_of(i + 1) + h, (i + 1) % a.ntiles, t, xn);
-    if (GATHER && tt == 0) {
-      for (int b = tid; b < a.nb; b += NT) sa[b] = Vec<NC>::zero();
-    }
+    if (i + 1 < nitems) load_tile<K2>(a, col_of(i + 1), (i + 1) % a.ntiles, t, xn);
     phase0_stages<K2>(x);
     if constexpr (K2 > 4) {
 #pragma unroll
-      for (int v = 0; v < 16; ++v) ex[h * kE + Geo<K2>::p0(t, v)] = x[v];
+      for (int v = 0; v < 16; ++v) ex[Geo<K2>::p0(t, v)] = x[v];
       __syncthreads();
 #pragma unroll
-      for (int v = 0; v < 16; ++v) x[v] = ex[h * kE + Geo<K2>::p1(t, v)];
+      for (int v = 0; v < 16; ++v) x[v] = ex[Geo<K2>::p1(t, v)];
       phase1_stages<K2>(x);
+      __syncthreads();  // ex is rewritten by the next item
     }
-    if (!GATHER) {
-      const int64_t col = NC * grp + h;
-      if (col < a.ncols) {
-        double* dst = a.Y + col * a.ldy;
+    if (col < a.ncols) {
+      double* dst = a.Y + col * a.ldy;
 #pragma unroll
-        for (int v = 0; v < 16; ++v) {
-          const int p = Geo<K2>::pf(t, v);
-          const int64_t r = tile_row(tt, p, K2, a.lo);
-          if (r < a.nvalid) dst[r] = x[v];
-        }
+      for (int v = 0; v < 16; ++v) {
+        const int64_t r = tile_row(tt, Geo<K2>::pf(t, v), K2, a.lo);
+        if (r < a.nvalid) dst[r] = x[v];
       }
-      if constexpr (K2 > 4) __syncthreads();  // ex is rewritten by the next item
-      continue;
-    }
-    __syncthreads();  // exchange reads done (K2 > 4) / previous walk done
-#pragma unroll
-    for (int v = 0; v < 16; ++v) {
-      const int p = Geo<K2>::pf(t, v);
-      reinterpret_cast<double*>(tile)[NC * p + h] = x[v];
-    }
-    asm volatile("cp.async.wait_all;\n" ::);
-    __syncthreads();
-    // rank rounds: every entry of round rho hits a distinct bucket
-    for (int rho = 0; rho < kRounds; ++rho) {
-      const int e0 = sroff[rho], e1 = sroff[rho + 1];
-      if (e0 == e1) break;
-      if (rho < kRounds - 1) {
-        // entries of one round hit distinct buckets: kU of them in flight per thread
-        constexpr int kU = 4;
-        for (int e = e0 + tid; e < e1; e += kU * NT) {
-          uint32_t w[kU];
-          int bk[kU];
-          V v[kU], acc[kU];
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int eu = e + u * NT;
-            w[u] = eu < e1 ? slst[eu] : kPadWord;
-            bk[u] = (int)((w[u] >> kLE) & ((1u << kBucketBits) - 1)) - a.b0;
-          }
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            if ((unsigned)bk[u] < (unsigned)a.nb) {
-              v[u] = tile[w[u] & (kE - 1)];
-              acc[u] = sa[bk[u]];
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < kU; ++u)
-            if ((unsigned)bk[u] < (unsigned)a.nb) sa[bk[u]] = Vec<NC>::addsub(acc[u], v[u], w[u] >> 31);
-        }
-      } else if (tid == 0) {  // ranks >= kRounds - 1, in list (= per-bucket rank) order
-        for (int e = e0; e < e1; ++e) {
-          const uint32_t w = slst[e];
-          const int bk = (int)((w >> kLE) & ((1u << kBucketBits) - 1)) - a.b0;
-          if ((unsigned)bk < (unsigned)a.nb) sa[bk] = Vec<NC>::addsub(sa[bk], tile[w & (kE - 1)], w >> 31);
-        }
-      }
-      __syncthreads();
-    }
-    __syncthreads();  // every thread is past its last read of sroff / slst
-    if (i + 1 < nitems) issue_list((i + 1) % a.ntiles);
-    if (tt == a.ntiles - 1) {  // column group done: SA columns out
-      for (int hh = 0; hh < NC; ++hh) {
-        const int64_t c = NC * grp + hh;
-        if (c >= a.ncols) break;
-        double* o = c < a.ncolSA ? a.SA + c * a.ldsa : a.Sb;
-        for (int b = tid; b < a.nb; b += NT) o[a.b0 + b] = a.alpha * Vec<NC>::get(sa[b], hh);
-      }
-      __syncthreads();  // sa is zeroed by the next group
     }
   }
 }
 
-// Warp-specialised pass 2 (GATHER, one column per CTA at a time, 512 threads):
-// warps 0-7 produce -- load a tile, butterflies, the final values into tile
-// buffer b (and the tile's list into list buffer b) -- while warps 8-15 consume
-// the other buffer with the rank rounds.  The halves meet only at named
-// barriers: FULL[b] (producers arrive, consumers wait) and EMPTY[b] (consumers
-// arrive, producers wait); the exchange and the rank rounds each use a barrier
-// of their own half.  Same arithmetic and order as cm_pass2_kernel.
+// ------------------------------------------------------------------ fused final pass: owner plan
+// The final pass applies the last K2 butterfly stages to a 4096-position tile
+// and adds every final value into the column's sketch, which stays in shared
+// memory while one CTA sweeps the column.  Determinism without atomics comes
+// from OWNERSHIP: the rows of a tile are the same for every column, so a plan
+// built once per sketch (cm_plan_kernel) hands every bucket that the tile hits
+// to exactly one consumer thread, together with all of that bucket's entries
+// of the tile in ascending position order.  A thread adds its entries one after
+// the other (a read-modify-write of its own buckets, no other thread touches
+// them during the tile); tiles are separated by one barrier.  A bucket thus
+// receives the rows of each tile in ascending order, tile after tile -- the
+// fixed order of DESIGN.md R17 -- with no rank rounds.
+//
+// Consumer thread c handles bucket class c & 15 (bucket = 16 kb + class), so
+// the 16 lanes of a half-warp always address 16 distinct shared-memory banks of
+// the sketch; the plan balances a class's entries over its 16 threads
+// (slot u = 2 (c >> 5) + ((c >> 4) & 1)).
+//
+// Plan word: bits 0-11 position p in the tile, 12-27 kb (serial list: the local
+// bucket), 28 first entry of its bucket in this thread's tile list, 29 valid
+// (serial list only), 30 last entry of its bucket, 31 sign.  Padding words are 0.
+// A tile's plan holds J steps (a multiple of 8) per consumer thread, stored as
+// uint4 quads [j / 4][thread]; padding words are 0 (invalid), and the
+// consumer predicates them off instead of branching.
+constexpr int kNP = 256;  // producer threads (load, butterflies, stage)
+constexpr int kNC = 256;  // consumer threads (owner adds)
+constexpr int kNBuf = 2;  // staged tiles
+constexpr uint32_t kHead = 1u << 28, kValid = 1u << 29, kLast = 1u << 30, kNeg = 1u << 31;
+constexpr uint32_t kKbMask = (1u << 16) - 1;
+
+__host__ __device__ constexpr int plan_jcap(int s) { return 24 * s + 16; }  // multiple of 4
+__host__ __device__ constexpr int64_t plan_tile_words(int s) { return (int64_t)plan_jcap(s) * kNC; }
+__host__ __device__ constexpr int nb_pad(int nb) { return (nb + 15) & ~15; }
+__host__ __device__ __forceinline__ int64_t plan_index(int j, int c) { return ((int64_t)(j >> 2) * kNC + c) * 4 + (j & 3); }
+
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nbar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-constexpr int kBarProd = 1, kBarCons = 2, kBarFull = 3, kBarEmpty = 5;
-// consumer threads: 384 measured slower than 256 (C3HD pass 2 3.52 vs 3.39 ms,
-// C5 40.8 vs 39.4 ms) -- the halves share the shared-memory pipe, not threads
-#ifndef SKH_WS_CONS
-#define SKH_WS_CONS 256
-#endif
-constexpr int kRoffPad = 48;
+constexpr int kBarProd = 1, kBarCons = 2, kBarFull = 3, kBarEmpty = 3 + kNBuf;
 
-__host__ __device__ constexpr size_t ws_smem_bytes(int s, int nb) {
-  return 2 * (size_t)kE * 8 + 2 * (size_t)4 * list_cap(s) + 2 * sizeof(int32_t) * kRoffPad + 8 * (size_t)nb;
+// cm_plan_kernel: sorted entries (4 B per entry) + class-major counters
+__host__ __device__ constexpr size_t plan_smem_bytes(int s, int nb) {
+  return (size_t)4 * kE * s + sizeof(int) * (size_t)nb_pad(nb) + 16;
+}
+__host__ __device__ constexpr size_t gather_smem_bytes(int nb) {
+  return (size_t)kNBuf * kE * 8 + 8 * (size_t)nb_pad(nb);
 }
 
-template <int K2, int CONS>
-__global__ void __launch_bounds__(256 + CONS, 1) cm_pass2_ws_kernel(const PassArgs a) {
-  constexpr int NALL = 256 + CONS;
+// Warp-specialised (one CTA per SM, 512 threads): warps 0-7 produce -- load a
+// tile (the next one is in flight in registers), run its butterflies (one
+// exchange through the staging buffer when K2 > 4), leave the final values in
+// staging buffer b -- while warps 8-15 consume the other buffer with the owner
+// plan.  FULL[b] / EMPTY[b] named barriers hand the buffers over.
+template <int K2>
+__global__ void __launch_bounds__(kNP + kNC, 1) cm_gather_kernel(const PassArgs a) {
+  constexpr int NALL = kNP + kNC;
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int cap = list_cap(a.s);
-  double* buf = reinterpret_cast<double*>(smraw);                                   // [2][kE]
-  uint32_t* lst = reinterpret_cast<uint32_t*>(smraw + 2 * (size_t)kE * 8);          // [2][cap]
-  int32_t* ro = reinterpret_cast<int32_t*>(smraw + 2 * (size_t)kE * 8 + 2 * (size_t)4 * cap);  // [2][kRoffPad]
-  double* sa = reinterpret_cast<double*>(smraw + 2 * (size_t)kE * 8 + 2 * (size_t)4 * cap +
-                                         2 * sizeof(int32_t) * kRoffPad);  // [nb]
+  double* buf = reinterpret_cast<double*>(smraw);                             // [kNBuf][kE]
+  double* sa = reinterpret_cast<double*>(smraw + (size_t)kNBuf * kE * 8);    // [nb_pad + 16]
   const int tid = threadIdx.x;
-  const bool producer = tid < 256;
-  const int t = producer ? tid : tid - 256;
   const int64_t my_cols = a.ncols > blockIdx.x ? (a.ncols - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t nitems = my_cols * a.ntiles;
-  auto col_of = [&](int64_t i) { return (int64_t)blockIdx.x + (i / a.ntiles) * gridDim.x; };
-  if (producer) {
+  // items i = (column, tile) in order: this CTA's columns blockIdx.x, + gridDim.x, ...
+  if (tid < kNP) {
+    const int t = tid;
     double x[16], xn[16];
-    if (nitems > 0) load_tile<K2>(a, col_of(0), 0, t, xn);
+    int64_t ncol = blockIdx.x, ntt = 0;  // the item whose loads are in flight
+    if (nitems > 0) load_tile<K2>(a, ncol, ntt, t, xn);
     for (int64_t i = 0; i < nitems; ++i) {
-      const int b = (int)(i & 1);
-      const int64_t tt = i % a.ntiles;
+      const int b = (int)(i % kNBuf);
 #pragma unroll
       for (int v = 0; v < 16; ++v) x[v] = xn[v];
-      if (i + 1 < nitems) load_tile<K2>(a, col_of(i + 1), (i + 1) % a.ntiles, t, xn);
-      phase0_stages<K2>(x);
-      if (i >= 2) nbar_sync(kBarEmpty + b, NALL);  // the consumers are done with buffer b
-      double* ex = buf + (size_t)b * kE;
-      // this tile's list and round offsets into list buffer b
-      const uint4* gl = reinterpret_cast<const uint4*>(a.lists + tt * (int64_t)cap);
-      uint32_t* dl = lst + (size_t)b * cap;
-      for (int k = t; k < cap / 4; k += 256) {
-        const unsigned dsts = (unsigned)__cvta_generic_to_shared(dl + 4 * k);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dsts), "l"(gl + k));
+      if (++ntt == a.ntiles) {
+        ntt = 0;
+        ncol += gridDim.x;
       }
-      asm volatile("cp.async.commit_group;\n" ::);
-      if (t < kRounds + 1) ro[b * kRoffPad + t] = a.roff[tt * kRoffStride + t];
+      if (i + 1 < nitems) load_tile<K2>(a, ncol, ntt, t, xn);
+      phase0_stages<K2>(x);
+      if (i >= kNBuf) nbar_sync(kBarEmpty + b, NALL);  // the consumers are done with buffer b
+      double* ex = buf + (size_t)b * kE;
       if constexpr (K2 > 4) {
 #pragma unroll
         for (int v = 0; v < 16; ++v) ex[Geo<K2>::p0(t, v)] = x[v];
-        nbar_sync(kBarProd, 256);
+        nbar_sync(kBarProd, kNP);
 #pragma unroll
         for (int v = 0; v < 16; ++v) x[v] = ex[Geo<K2>::p1(t, v)];
         phase1_stages<K2>(x);
-        nbar_sync(kBarProd, 256);  // exchange reads done before the final values overwrite it
+        nbar_sync(kBarProd, kNP);  // exchange reads done before the final values overwrite it
       }
 #pragma unroll
       for (int v = 0; v < 16; ++v) ex[Geo<K2>::pf(t, v)] = x[v];
-      asm volatile("cp.async.wait_all;\n" ::);
       nbar_arrive(kBarFull + b, NALL);
     }
-  } else {
-    for (int64_t i = 0; i < nitems; ++i) {
-      const int b = (int)(i & 1);
-      const int64_t tt = i % a.ntiles, col = col_of(i);
-      if (tt == 0) {
-        for (int k = t; k < a.nb; k += CONS) sa[k] = 0.0;
-        nbar_sync(kBarCons, CONS);
-      }
-      nbar_sync(kBarFull + b, NALL);
-      const double* tile = buf + (size_t)b * kE;
-      const uint32_t* slst = lst + (size_t)b * cap;
-      const int32_t* sroff = ro + b * kRoffPad;
-      for (int rho = 0; rho < kRounds; ++rho) {
-        const int e0 = sroff[rho], e1 = sroff[rho + 1];
-        if (e0 == e1) break;
-        if (rho < kRounds - 1) {
-          constexpr int kU = 4;
-          for (int e = e0 + t; e < e1; e += kU * CONS) {
-            uint32_t w[kU];
-            int bk[kU];
-            double v[kU], acc[kU];
+    return;
+  }
+  // ---- consumers: blocks of up to JB plan steps per thread (6 uint4 of words),
+  // the next block in flight in registers while the current one is added
+  constexpr int JB = 24;
+  const int c = tid - kNP, cls = c & 15;
+  const int64_t tw4 = plan_tile_words(a.s) / 4;
+  const uint4* w4 = reinterpret_cast<const uint4*>(a.words) + c;
+  const uint4 dq = make_uint4(0u, 0u, 0u, 0u);  // words past J: invalid (predicated off)
+  auto load_block = [&](int64_t tt, int bk, int J8, uint4 (&dst)[6]) {
+    const uint4* p = w4 + tt * tw4 + (int64_t)bk * (JB / 4) * kNC;
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
-              const int eu = e + u * CONS;
-              w[u] = eu < e1 ? slst[eu] : kPadWord;
-              bk[u] = (int)((w[u] >> kLE) & ((1u << kBucketBits) - 1)) - a.b0;
-            }
+    for (int q = 0; q < 6; ++q) dst[q] = bk * JB + 4 * q < J8 ? __ldg(p + q * kNC) : dq;
+  };
+  uint4 cw[6], nw[6];
+  double run = 0.0;  // running value of the open bucket run (it may continue into the next group of 4)
+  double* sac = sa + cls;  // this thread's bucket class: k = 16 kb + cls
+  int Jc = nitems > 0 ? __ldg(a.hdr + 0) : 0;
+  if (Jc > 0) load_block(0, 0, Jc, nw);
+  int64_t col = blockIdx.x, tt = 0;
+  for (int64_t i = 0; i < nitems; ++i) {
+    const int b = (int)(i % kNBuf);
+    const int64_t ttn = tt + 1 == a.ntiles ? 0 : tt + 1;
+    if (tt == 0) {
+      for (int k = c; k < a.nb; k += kNC) sa[k] = 0.0;
+      nbar_sync(kBarCons, kNC);
+    }
+    const int Jn = i + 1 < nitems ? __ldg(a.hdr + ttn) : 0;
+    const int nbk = Jc > 0 ? (Jc + JB - 1) / JB : 0;
+    nbar_sync(kBarFull + b, NALL);
+    const double* tile = buf + (size_t)b * kE;
+    for (int bk = 0; bk < nbk; ++bk) {
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
-              if ((unsigned)bk[u] < (unsigned)a.nb) {
-                v[u] = tile[w[u] & (kE - 1)];
-                acc[u] = sa[bk[u]];
-              }
-            }
+      for (int q = 0; q < 6; ++q) cw[q] = nw[q];
+      if (bk + 1 < nbk) load_block(tt, bk + 1, Jc, nw);
+      else if (Jn > 0) load_block(ttn, 0, Jn, nw);
+      const int steps = min(JB, Jc - bk * JB);
 #pragma unroll
-            for (int u = 0; u < kU; ++u)
-              if ((unsigned)bk[u] < (unsigned)a.nb) sa[bk[u]] = (w[u] >> 31) ? acc[u] - v[u] : acc[u] + v[u];
-          }
-        } else if (t == 0) {
-          for (int e = e0; e < e1; ++e) {
-            const uint32_t w = slst[e];
-            const int bk = (int)((w >> kLE) & ((1u << kBucketBits) - 1)) - a.b0;
-            if ((unsigned)bk < (unsigned)a.nb) sa[bk] = (w >> 31) ? sa[bk] - tile[w & (kE - 1)] : sa[bk] + tile[w & (kE - 1)];
-          }
+      for (int q = 0; q < 6; ++q) {
+        if (q * 4 >= steps) break;
+        const uint32_t w[4] = {cw[q].x, cw[q].y, cw[q].z, cw[q].w};
+        // a bucket's entries of the tile are consecutive in the thread's list and
+        // are added in ascending row order with the running value kept in a
+        // register: one shared-memory read at the head, one write at the last
+        // entry (the order is that of one add per entry).  Padding words are 0:
+        // they read tile[0] (a broadcast) and neither load nor store the sketch.
+        double v[4], a0[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          v[u] = tile[w[u] & (kE - 1)];
+          if (w[u] & kHead) a0[u] = sac[(w[u] >> 12 & kKbMask) << 4];
         }
-        nbar_sync(kBarCons, CONS);
-      }
-      if (i + 2 < nitems) nbar_arrive(kBarEmpty + b, NALL);  // buffer b free (no arrival left unmatched)
-      if (tt == a.ntiles - 1) {  // column done: SA column out (the last round ended with a consumer barrier)
-        if (col < a.ncols) {
-          double* o = col < a.ncolSA ? a.SA + col * a.ldsa : a.Sb;
-          for (int k = t; k < a.nb; k += CONS) o[a.b0 + k] = a.alpha * sa[k];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double x = __hiloint2double(__double2hiint(v[u]) ^ (int)(w[u] & kNeg), __double2loint(v[u]));
+          run = ((w[u] & kHead) ? a0[u] : run) + x;
+          if (w[u] & kLast) sac[(w[u] >> 12 & kKbMask) << 4] = run;
         }
-        nbar_sync(kBarCons, CONS);  // sa is zeroed for the next column
       }
     }
+    if (nbk == 0 && Jn > 0) load_block(ttn, 0, Jn, nw);
+    if (Jc < 0 && c == 0) {  // serial list (a tile whose buckets could not be balanced), ascending entry order
+      const uint32_t* sl = a.words + tt * plan_tile_words(a.s);
+      for (int e = 0; e < -Jc; ++e) {
+        const uint32_t x = __ldg(sl + e);
+        if (!(x & kValid)) continue;
+        const int k = (int)((x >> 12) & kKbMask);
+        const double vv = tile[x & (kE - 1)];
+        sa[k] = (x & kNeg) ? sa[k] - vv : sa[k] + vv;
+      }
+    }
+    nbar_sync(kBarCons, kNC);                                   // every add of this tile is done
+    if (i + kNBuf < nitems) nbar_arrive(kBarEmpty + b, NALL);  // buffer b free (no arrival left unmatched)
+    if (tt == a.ntiles - 1 && col < a.ncols) {                  // column done: SA column out
+      double* o = col < a.ncolSA ? a.SA + col * a.ldsa : a.Sb;
+      // same k -> thread map as the zeroing above, so no barrier is needed before the next column's zeroing
+      for (int k = c; k < a.nb; k += kNC) o[a.b0 + k] = a.alpha * sa[k];
+    }
+    Jc = Jn;
+    if (ttn == 0) col += gridDim.x;
+    tt = ttn;
   }
+}
+
+// ------------------------------------------------------------------ owner plan (once per sketch)
+// One CTA per tile.  (1) count the tile's entries per local bucket k, keyed
+// class-major (o = (k & 15) nkb + (k >> 4)); (2) exclusive scan; (3) place the
+// entries (atomic slot claims), then sort every bucket run by entry index e =
+// p s + q -- a run is tiny and the sorted result is unique, so the plan does not
+// depend on the order of the claims; (4) split each class's runs over its 16
+// slots (runs are never split); (5) write the words, [step j][consumer thread].
+// A tile whose longest slot exceeds plan_jcap(s) steps (only for very small m)
+// becomes a serial list in ascending e.
+__device__ __forceinline__ int block_excl_scan_256(int v, int* tmp, int& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < 8 ? tmp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < 8) tmp[8 + lane] = t;
+  }
+  __syncthreads();
+  total = tmp[15];
+  const int r = (w > 0 ? tmp[8 + w - 1] : 0) + x - v;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256) cm_plan_kernel(const int32_t* __restrict__ col_rows,
+                                                      const int8_t* __restrict__ col_signs, int s, int K2, int lo,
+                                                      int64_t nvalid, int b0, int nb, uint32_t* __restrict__ words,
+                                                      int32_t* __restrict__ hdr) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ int tmp[16];
+  __shared__ int bnd[16][17];
+  __shared__ int cstart[17];
+  __shared__ int jmax;
+  const int tid = threadIdx.x;
+  const int64_t tt = blockIdx.x;
+  const int E = kE * s;
+  const int nkb = (nb + 15) >> 4;
+  const int no = 16 * nkb;
+  uint32_t* sorted = reinterpret_cast<uint32_t*>(smraw);        // [E]: e | kb << 15 | neg << 31
+  int* off = reinterpret_cast<int*>(smraw + sizeof(uint32_t) * E);  // [no]
+  for (int o = tid; o < no; o += 256) off[o] = 0;
+  if (tid == 0) jmax = 0;
+  __syncthreads();
+  auto entry = [&](int e, int& k, int& neg) {  // local bucket of entry e (-1: none in this launch)
+    const int p = e / s, q = e - p * s;
+    const int64_t r = tile_row(tt, p, K2, lo);
+    k = -1;
+    neg = 0;
+    if (r < nvalid) {
+      const int bk = col_rows[r * s + q] - b0;
+      if ((unsigned)bk < (unsigned)nb) {
+        k = bk;
+        neg = col_signs[r * s + q] < 0;
+      }
+    }
+  };
+  // (1) counts
+  for (int e = tid; e < E; e += 256) {
+    int k, neg;
+    entry(e, k, neg);
+    if (k >= 0) atomicAdd(&off[(k & 15) * nkb + (k >> 4)], 1);
+  }
+  __syncthreads();
+  // (2) exclusive scan over o: contiguous segments per thread
+  const int seg = (no + 255) / 256, o0 = min(no, tid * seg), o1 = min(no, o0 + seg);
+  int sum = 0;
+  for (int o = o0; o < o1; ++o) sum += off[o];
+  int total;
+  int run = block_excl_scan_256(sum, tmp, total);
+  for (int o = o0; o < o1; ++o) {
+    const int cnt = off[o];
+    off[o] = run;
+    run += cnt;
+  }
+  __syncthreads();
+  if (tid < 16) cstart[tid] = off[tid * nkb];
+  if (tid == 0) cstart[16] = total;
+  __syncthreads();
+  // (3) place (off[o] advances to the end of run o), then sort runs by e
+  for (int e = tid; e < E; e += 256) {
+    int k, neg;
+    entry(e, k, neg);
+    if (k >= 0) {
+      const int pos = atomicAdd(&off[(k & 15) * nkb + (k >> 4)], 1);
+      sorted[pos] = (uint32_t)e | ((uint32_t)(k >> 4) << 15) | ((uint32_t)neg << 31);
+    }
+  }
+  __syncthreads();
+  for (int o = tid; o < no; o += 256) {
+    const int r0 = o == 0 ? 0 : off[o - 1], r1 = off[o];
+    for (int i = r0 + 1; i < r1; ++i) {  // insertion sort by e (low 15 bits)
+      const uint32_t x = sorted[i];
+      int j = i - 1;
+      while (j >= r0 && (sorted[j] & 0x7FFFu) > (x & 0x7FFFu)) {
+        sorted[j + 1] = sorted[j];
+        --j;
+      }
+      sorted[j + 1] = x;
+    }
+  }
+  __syncthreads();
+  // (4) slots: thread (cl, u) starts at the first run start at or after u T
+  const int cl = tid & 15, u = tid >> 4;
+  const int cs = cstart[cl], C = cstart[cl + 1] - cs;
+  const int T = (C + 15) / 16;
+  {
+    int i = min(u * T, C);
+    while (i > 0 && i < C && ((sorted[cs + i] >> 15) & 0xFFFFu) == ((sorted[cs + i - 1] >> 15) & 0xFFFFu)) ++i;
+    bnd[cl][u] = i;
+    if (u == 15) bnd[cl][16] = C;
+  }
+  __syncthreads();
+  const int i0 = bnd[cl][u], cnt = bnd[cl][u + 1] - i0;
+  atomicMax(&jmax, cnt);
+  __syncthreads();
+  const int J8 = (jmax + 3) & ~3;  // steps: a multiple of 4 (one uint4 of words)
+  uint32_t* out = words + tt * plan_tile_words(s);
+  if (J8 > plan_jcap(s)) {  // serial list in ascending e
+    for (int e = tid; e < E; e += 256) {
+      int k, neg;
+      entry(e, k, neg);
+      out[e] = k < 0 ? 0u : ((uint32_t)(e / s) | ((uint32_t)k << 12) | kValid | ((uint32_t)neg << 31));
+    }
+    if (tid == 0) hdr[tt] = -E;
+    return;
+  }
+  // (5) words: the thread's runs in order, each run's entries in ascending e,
+  // flagged head (first of its bucket) and last
+  const uint32_t* mine = sorted + cs + i0;
+  const int c = 32 * (u >> 1) + 16 * (u & 1) + cl;  // consumer thread of (class cl, slot u)
+  for (int j = 0; j < J8; ++j) {
+    uint32_t wd = 0;
+    if (j < cnt) {
+      const uint32_t x = mine[j];
+      const uint32_t kb = (x >> 15) & 0xFFFFu;
+      const bool head = j == 0 || ((mine[j - 1] >> 15) & 0xFFFFu) != kb;
+      const bool last = j + 1 == cnt || ((mine[j + 1] >> 15) & 0xFFFFu) != kb;
+      wd = (uint32_t)((x & 0x7FFFu) / s) | (kb << 12) | (x & 0x80000000u) | (head ? kHead : 0u) | (last ? kLast : 0u);
+    }
+    out[plan_index(j, c)] = wd;
+  }
+  if (tid == 0) hdr[tt] = J8;
 }
 
 int g_nsm = 0;
@@ -595,316 +693,49 @@ int set_smem(F* f, size_t bytes) {
   return SKH_OK;
 }
 
-// ------------------------------------------------------------------ launch helpers
-// ------------------------------------------------------------------ tile lists
-// One warp per tile.  Entries e = p s + q (q = draw) in ascending e; the rank of
-// an entry is the number of earlier entries of the tile in the same bucket
-// (warp __match_any_sync + per-bucket counters in shared memory, so it is
-// deterministic).  Rank group rho (ranks clamped to kRounds - 1) occupies
-// [roff[rho], roff[rho+1]).  Within a group the buckets are distinct, so the
-// order is free: slot off + ncls i + c holds the i-th entry whose bucket is = c
-// (mod ncls), empty slots are kPadWord.  With ncls = 16 (one column per CTA,
-// 8-byte SA entries) every half-warp, and with ncls = 8 (column pairs, 16-byte
-// entries) every quarter-warp, then addresses distinct banks of the SA.  A tile whose padded groups would exceed list_cap(s) keeps the
-// plain ascending-e order instead (correct, only slower).
-__global__ void cm_lists_kernel(const int32_t* __restrict__ col_rows, const int8_t* __restrict__ col_signs, int s,
-                                int64_t m, int K2, int lo, int64_t nvalid, int ncls, uint32_t* __restrict__ lists,
-                                int32_t* __restrict__ roff) {
-  extern __shared__ unsigned char smraw[];
-  int32_t* hist = reinterpret_cast<int32_t*>(smraw);      // [32][16]
-  int32_t* cur = hist + 512;                              // [32][16]
-  int32_t* off = cur + 512;                               // [34]: offsets + padded flag
-  uint16_t* cnt = reinterpret_cast<uint16_t*>(smraw + 8192);  // [m]
-  const int lane = threadIdx.x;
-  const int64_t tt = blockIdx.x;
-  const unsigned lt = (1u << lane) - 1u;
-  const int cap = list_cap(s);
-  uint32_t* out = lists + tt * (int64_t)cap;
-  const int ne = kE * s;
-  bool padded = true;
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int64_t b = lane; b < m; b += 32) cnt[b] = 0;
-    if (pass == 0)
-      for (int i = lane; i < 512; i += 32) hist[i] = 0;
-    __syncwarp();
-    for (int e0 = 0; e0 < ne; e0 += 32) {
-      const int e = e0 + lane;
-      const int p = e / s, q = e - p * s;
-      const int64_t r = tile_row(tt, p, K2, lo);
-      const bool valid = r < nvalid;
-      if (__ballot_sync(0xffffffffu, valid) == 0u) continue;
-      int bk = -1, neg = 0;
-      if (valid) {
-        bk = col_rows[r * s + q];
-        neg = col_signs[r * s + q] < 0;
-      }
-      const unsigned grp = __match_any_sync(0xffffffffu, bk);
-      const int base = valid ? (int)cnt[bk] : 0;
-      __syncwarp();
-      const int rank = base + __popc(grp & lt);
-      if (valid && ((grp >> lane) >> 1) == 0u) cnt[bk] = (uint16_t)(base + __popc(grp));
-      __syncwarp();
-      const int rk = min(rank, kRounds - 1);
-      const int key = rk * 16 + (padded ? (bk & (ncls - 1)) : 0);
-      if (pass == 0) {
-        if (valid) atomicAdd(&hist[rk * 16 + (bk & (ncls - 1))], 1);
-      } else {
-        const unsigned g2 = __match_any_sync(0xffffffffu, valid ? key : -1);
-        const int idx = valid ? cur[key] + __popc(g2 & lt) : 0;
-        __syncwarp();
-        if (valid && ((g2 >> lane) >> 1) == 0u) cur[key] += __popc(g2);
-        __syncwarp();
-        if (valid) {
-          const int slot = padded ? off[rk] + ncls * idx + (bk & (ncls - 1)) : off[rk] + idx;
-          out[slot] = (uint32_t)p | ((uint32_t)bk << kLE) | ((uint32_t)neg << 31);
-        }
-      }
-    }
-    __syncwarp();
-    if (pass == 0) {
-      if (lane == 0) {
-        int acc = 0;
-        for (int i = 0; i < kRounds; ++i) {  // padded group lengths
-          int mx = 0;
-          for (int c = 0; c < ncls; ++c) mx = max(mx, hist[i * 16 + c]);
-          off[i] = acc;
-          acc += ncls * mx;
-        }
-        off[kRounds] = acc;
-        if (acc > cap) {  // plain order
-          acc = 0;
-          for (int i = 0; i < kRounds; ++i) {
-            int t = 0;
-            for (int c = 0; c < ncls; ++c) t += hist[i * 16 + c];
-            off[i] = acc;
-            acc += t;
-          }
-          off[kRounds] = acc;
-          off[kRounds + 1] = 0;
-        } else {
-          off[kRounds + 1] = 1;
-        }
-        for (int i = 0; i <= kRounds; ++i) roff[tt * kRoffStride + i] = off[i];
-      }
-      __syncwarp();
-      padded = off[kRounds + 1] != 0;
-      for (int i = lane; i < 512; i += 32) cur[i] = 0;
-      if (padded)
-        for (int i = lane; i < off[kRounds]; i += 32) out[i] = kPadWord;
-      __syncwarp();
-    }
-  }
-}
 
-// The same lists from W warps per tile (W <= 8, limited by W per-warp bucket
-// counters of m uint16 in shared memory): the tile's entries are cut into W
-// contiguous segments; (1) each warp counts its segment's buckets; (2) a
-// prefix over warps gives every warp the number of earlier same-bucket entries,
-// so it ranks its segment exactly as the one-warp walk would, adding to the
-// rank-group histogram and to per-warp key counts; (3) prefixes of those
-// counts give every warp its first slot per key, and a second ranking walk
-// places the entries.  The lists are identical to cm_lists_kernel's.
-__global__ void cm_lists_par_kernel(const int32_t* __restrict__ col_rows, const int8_t* __restrict__ col_signs,
-                                    int s, int64_t m, int K2, int lo, int64_t nvalid, int ncls,
-                                    uint32_t* __restrict__ lists, int32_t* __restrict__ roff) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int W = blockDim.x >> 5;
-  int32_t* hist = reinterpret_cast<int32_t*>(smraw);  // [512]
-  int32_t* off = hist + 512;                          // [64]: offsets + padded flag
-  int32_t* kcp = off + 64;                            // [W][512] key counts (padded keys)
-  int32_t* kcq = kcp + W * 512;                       // [W][32]  key counts (plain keys)
-  uint16_t* cntw = reinterpret_cast<uint16_t*>(kcq + W * 32);  // [W][m]
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t tt = blockIdx.x;
-  const unsigned lt = (1u << lane) - 1u;
-  const int cap = list_cap(s);
-  uint32_t* out = lists + tt * (int64_t)cap;
-  const int ne = kE * s, seg = ne / W, e_lo = w * seg, e_hi = e_lo + seg;
-  uint16_t* cnt = cntw + (int64_t)w * m;
-  for (int64_t b = lane; b < m; b += 32) cnt[b] = 0;
-  for (int i = lane; i < 512; i += 32) kcp[w * 512 + i] = 0;
-  kcq[w * 32 + lane] = 0;
-  for (int i = threadIdx.x; i < 512; i += blockDim.x) hist[i] = 0;
-  auto entry = [&](int e, int& bk, int& neg) {
-    const int p = e / s, q = e - p * s;
-    const int64_t r = tile_row(tt, p, K2, lo);
-    bk = -1;
-    neg = 0;
-    if (r < nvalid) {
-      bk = col_rows[r * s + q];
-      neg = col_signs[r * s + q] < 0;
-    }
-  };
-  __syncthreads();
-  // (1) per-warp bucket counts
-  for (int e0 = e_lo; e0 < e_hi; e0 += 32) {
-    int bk, neg;
-    entry(e0 + lane, bk, neg);
-    const unsigned grp = __match_any_sync(0xffffffffu, bk);
-    if (bk >= 0 && (grp & lt) == 0) cnt[bk] = (uint16_t)(cnt[bk] + __popc(grp));
-    __syncwarp();
-  }
-  __syncthreads();
-  for (int64_t b = threadIdx.x; b < m; b += blockDim.x) {  // exclusive prefix over warps
-    int run = 0;
-    for (int v = 0; v < W; ++v) {
-      const int c = cntw[(int64_t)v * m + b];
-      cntw[(int64_t)v * m + b] = (uint16_t)run;
-      run += c;
-    }
-  }
-  __syncthreads();
-  // (2) ranks -> rank-group histogram and per-warp key counts
-  for (int e0 = e_lo; e0 < e_hi; e0 += 32) {
-    int bk, neg;
-    entry(e0 + lane, bk, neg);
-    const bool valid = bk >= 0;
-    const unsigned grp = __match_any_sync(0xffffffffu, bk);
-    const int base = valid ? (int)cnt[bk] : 0;
-    __syncwarp();
-    const int rank = base + __popc(grp & lt);
-    if (valid && (grp & lt) == 0) cnt[bk] = (uint16_t)(base + __popc(grp));
-    __syncwarp();
-    if (valid) {
-      const int rk = min(rank, kRounds - 1);
-      atomicAdd(&hist[rk * 16 + (bk & (ncls - 1))], 1);
-      atomicAdd(&kcp[w * 512 + rk * 16 + (bk & (ncls - 1))], 1);
-      atomicAdd(&kcq[w * 32 + rk], 1);
-    }
-  }
-  __syncthreads();
-  for (int64_t b = threadIdx.x; b < m; b += blockDim.x) {  // counters back to the prefixes
-    for (int v = W - 1; v >= 1; --v) cntw[(int64_t)v * m + b] = cntw[(int64_t)(v - 1) * m + b];
-    cntw[b] = 0;
-  }
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int i = 0; i < kRounds; ++i) {  // padded group lengths
-      int mx = 0;
-      for (int c = 0; c < ncls; ++c) mx = max(mx, hist[i * 16 + c]);
-      off[i] = acc;
-      acc += ncls * mx;
-    }
-    off[kRounds] = acc;
-    if (acc > cap) {  // plain order
-      acc = 0;
-      for (int i = 0; i < kRounds; ++i) {
-        int t = 0;
-        for (int c = 0; c < ncls; ++c) t += hist[i * 16 + c];
-        off[i] = acc;
-        acc += t;
-      }
-      off[kRounds] = acc;
-      off[kRounds + 1] = 0;
-    } else {
-      off[kRounds + 1] = 1;
-    }
-    for (int i = 0; i <= kRounds; ++i) roff[tt * kRoffStride + i] = off[i];
-  }
-  __syncthreads();
-  const bool padded = off[kRounds + 1] != 0;
-  // per-warp first slot index per key: exclusive prefix over warps
-  for (int key = threadIdx.x; key < 512; key += blockDim.x) {
-    int run = 0;
-    for (int v = 0; v < W; ++v) {
-      int* c = padded ? &kcp[v * 512 + key] : (key < 32 ? &kcq[v * 32 + key] : nullptr);
-      if (!c) break;
-      const int x = *c;
-      *c = run;
-      run += x;
-    }
-  }
-  if (padded)
-    for (int i = threadIdx.x; i < off[kRounds]; i += blockDim.x) out[i] = kPadWord;
-  __syncthreads();
-  // (3) rank again and place
-  int32_t* cur = padded ? kcp + w * 512 : kcq + w * 32;
-  for (int e0 = e_lo; e0 < e_hi; e0 += 32) {
-    const int e = e0 + lane;
-    int bk, neg;
-    entry(e, bk, neg);
-    const bool valid = bk >= 0;
-    const unsigned grp = __match_any_sync(0xffffffffu, bk);
-    const int base = valid ? (int)cnt[bk] : 0;
-    __syncwarp();
-    const int rank = base + __popc(grp & lt);
-    if (valid && (grp & lt) == 0) cnt[bk] = (uint16_t)(base + __popc(grp));
-    __syncwarp();
-    const int rk = min(rank, kRounds - 1);
-    const int key = padded ? rk * 16 + (bk & (ncls - 1)) : rk;
-    const unsigned g2 = __match_any_sync(0xffffffffu, valid ? key : -1);
-    const int idx = valid ? cur[key] + __popc(g2 & lt) : 0;
-    __syncwarp();
-    if (valid && (g2 & lt) == 0) cur[key] += __popc(g2);
-    __syncwarp();
-    if (valid) {
-      const int slot = padded ? off[rk] + ncls * idx + (bk & (ncls - 1)) : off[rk] + idx;
-      out[slot] = (uint32_t)(e / s) | ((uint32_t)bk << kLE) | ((uint32_t)neg << 31);
-    }
-  }
-}
-
-// Warp-specialised pass 2 where it measured faster: C3HD (K2 = 4, s = 2) pass 2
-// 4.48 -> 3.39 ms; C2 (K2 = 3, s = 1) equal; C5 (K2 = 8, s = 1) 38.5 -> 39.4 ms,
-// so the 8-bit exchange case keeps the two-CTA kernel.  SKH_CM_WS=0/1 forces.
-bool use_ws(int K2, int s) {
-  static const int forced = [] {
-    const char* e = getenv("SKH_CM_WS");
-    return e ? (e[0] == '1' ? 1 : 0) : -1;
-  }();
-  return forced >= 0 ? forced == 1 : (K2 <= 4 || s >= 2);
+template <int K2>
+int launch_mid_t(const PassArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)kE * 8;
+  auto* f = cm_mid_kernel<K2>;
+  int rc = set_smem(f, smem);
+  if (rc) return rc;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 256, smem);
+  const int64_t grid = std::min<int64_t>(a.ncols * a.ntiles, (int64_t)num_sms() * std::max(per_sm, 1));
+  if (grid < 1) return SKH_OK;
+  f<<<(unsigned)grid, 256, smem, st>>>(a);
+  note_launch();
+  return check_launch("cm_mid");
 }
 
 template <int K2>
-int launch_pass2_ws(const PassArgs& a, cudaStream_t st) {
-  const size_t smem = ws_smem_bytes(a.s, a.nb);
-  constexpr int CONS = SKH_WS_CONS;
-  auto* f = cm_pass2_ws_kernel<K2, CONS>;
+int launch_gather_t(const PassArgs& a, cudaStream_t st) {
+  const size_t smem = gather_smem_bytes(a.nb);
+  auto* f = cm_gather_kernel<K2>;
   int rc = set_smem(f, smem);
   if (rc) return rc;
   const int64_t grid = std::min<int64_t>(a.ncols, (int64_t)num_sms());
   if (grid < 1) return SKH_OK;
-  f<<<(unsigned)grid, 256 + CONS, smem, st>>>(a);
+  f<<<(unsigned)grid, kNP + kNC, smem, st>>>(a);
   note_launch();
-  return check_launch("cm_pass2_ws");
+  return check_launch("cm_gather");
 }
 
-template <int K2, bool GATHER, int NC>
-int launch_pass2_nc(const PassArgs& a, cudaStream_t st) {
-  if constexpr (GATHER && NC == 1) {
-    if (use_ws(K2, a.s) && ws_smem_bytes(a.s, a.nb) <= 227 * 1024) return launch_pass2_ws<K2>(a, st);
-  }
-  const size_t tileb = (size_t)NC * kE * 8;
-  const size_t smem = GATHER ? tileb + 256 + (size_t)4 * list_cap(a.s) + 8 * NC * (size_t)a.nb : tileb;
-  auto* f = cm_pass2_kernel<K2, GATHER, NC>;
-  int rc = set_smem(f, smem);
-  if (rc) return rc;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 256 * NC, smem);
-  if (per_sm < 1) {
-    set_error("cm pass 2: %zu bytes of shared memory do not fit an SM", smem);
-    return SKH_EINVAL;
-  }
-  const int64_t ngroups = (a.ncols + NC - 1) / NC;
-  const int64_t grid = std::min<int64_t>(ngroups, (int64_t)num_sms() * per_sm);
-  if (grid < 1) return SKH_OK;
-  f<<<(unsigned)grid, 256 * NC, smem, st>>>(a);
-  note_launch();
-  return check_launch("cm_pass2");
-}
-
-template <int K2, bool GATHER>
-int launch_pass2_t(const PassArgs& a, cudaStream_t st) {
-  return launch_pass2_nc<K2, GATHER, 1>(a, st);
+size_t plan_range_bytes(int64_t ntiles, int s) {
+  return align_up(sizeof(uint32_t) * (size_t)ntiles * (size_t)plan_tile_words(s)) +
+         align_up(sizeof(int32_t) * (size_t)ntiles);
 }
 
 }  // namespace
 
-// Largest bucket range one pass-2 launch accumulates on chip for draw count s
-// (one CTA per SM; smaller ranges let two CTAs share an SM).
+// Largest bucket range one fused-pass launch accumulates on chip (one CTA per
+// SM: the staged tiles + the sketch column in shared memory).
 int cm_max_buckets(int s) {
-  const size_t avail = 227 * 1024 - (size_t)kE * 8 - 256 - (size_t)4 * list_cap(s);
-  return s > 8 ? 0 : (int)(avail / 8);
+  if (s < 1 || s > 8) return 0;
+  const size_t avail = 227 * 1024 - (size_t)kNBuf * kE * 8;                // gather: staged tiles + SA
+  const size_t avail_plan = 227 * 1024 - (size_t)4 * kE * s - 16;           // plan: entries + counters
+  return (int)(std::min(avail / 8, avail_plan / 4) & ~(size_t)15);
 }
 
 // Pass 1 of columns of 2^L rows: bits [0, min(L, 13)).
@@ -963,56 +794,53 @@ int launch_cm_mid(double* Y, int64_t ldy, int64_t ncols, int64_t nrows, int lo, 
   a.ldy = ldy;
   a.s = 1;
   switch (K2) {
-    case 1: return launch_pass2_t<1, false>(a, st);
-    case 2: return launch_pass2_t<2, false>(a, st);
-    case 3: return launch_pass2_t<3, false>(a, st);
-    case 4: return launch_pass2_t<4, false>(a, st);
-    case 5: return launch_pass2_t<5, false>(a, st);
-    case 6: return launch_pass2_t<6, false>(a, st);
-    case 7: return launch_pass2_t<7, false>(a, st);
-    case 8: return launch_pass2_t<8, false>(a, st);
+    case 1: return launch_mid_t<1>(a, st);
+    case 2: return launch_mid_t<2>(a, st);
+    case 3: return launch_mid_t<3>(a, st);
+    case 4: return launch_mid_t<4>(a, st);
+    case 5: return launch_mid_t<5>(a, st);
+    case 6: return launch_mid_t<6>(a, st);
+    case 7: return launch_mid_t<7>(a, st);
+    case 8: return launch_mid_t<8>(a, st);
     default: set_error("cm mid pass: K2 = %d", K2); return SKH_EINVAL;
   }
 }
 
-size_t cm_lists_bytes(int64_t ntiles, int s) {
-  return align_up(sizeof(uint32_t) * (size_t)ntiles * list_cap(s)) +
-         align_up(sizeof(int32_t) * (size_t)ntiles * kRoffStride + 16);
+// Owner plans of the final pass, one per bucket range of at most
+// cm_max_buckets(s) buckets: [range][tile][plan_jcap(s)][kNC] words + [range][tile] steps.
+size_t cm_lists_bytes(int64_t ntiles, int s, int64_t m) {
+  const int cap = cm_max_buckets(s);
+  const int64_t nr = cap > 0 ? (m + cap - 1) / cap : 1;
+  return (size_t)nr * plan_range_bytes(ntiles, s);
 }
 
-// Tile lists of the final pass (bits [lo, lo + K2), or K2 = 0 row blocks).
+// Plans of the final pass (bits [lo, lo + K2), or K2 = 0 row blocks).
 int launch_cm_lists(const int32_t* col_rows, const int8_t* col_signs, int s, int64_t m, int K2, int lo,
                     int64_t nvalid, int64_t ntiles, void* lists_ws, cudaStream_t st) {
-  uint32_t* lists = static_cast<uint32_t*>(lists_ws);
-  int32_t* roff = reinterpret_cast<int32_t*>(static_cast<char*>(lists_ws) +
-                                             align_up(sizeof(uint32_t) * (size_t)ntiles * list_cap(s)));
-  const int ncls = 16;  // 8-byte SA entries: conflict-free half-warps
-  static const bool one_warp = [] {
-    const char* e = getenv("SKH_CM_LISTS_1W");
-    return e && e[0] == '1';
-  }();
-  // W warps per tile while W per-warp m-entry counters fit (<= 200 KB)
-  int W = 8;
-  while (W > 1 && (size_t)W * (sizeof(int32_t) * 544 + sizeof(uint16_t) * (size_t)m) + 2304 > 200 * 1024) W >>= 1;
-  if (!one_warp && W >= 2) {
-    const size_t smem = 2304 + (size_t)W * sizeof(int32_t) * 544 + align_up(sizeof(uint16_t) * (size_t)W * m, 16);
-    int rc = set_smem(cm_lists_par_kernel, smem);
-    if (rc) return rc;
-    cm_lists_par_kernel<<<(unsigned)ntiles, 32 * W, smem, st>>>(col_rows, col_signs, s, m, K2, lo, nvalid, ncls,
-                                                                 lists, roff);
-    note_launch();
-    return check_launch("cm_lists_par");
+  const int cap = cm_max_buckets(s);
+  if (cap < 1) {
+    set_error("column-major gather supports s <= 8");
+    return SKH_EINVAL;
   }
-  const size_t smem = 8192 + align_up(sizeof(uint16_t) * (size_t)m, 16);
-  int rc = set_smem(cm_lists_kernel, smem);
-  if (rc) return rc;
-  cm_lists_kernel<<<(unsigned)ntiles, 32, smem, st>>>(col_rows, col_signs, s, m, K2, lo, nvalid, ncls, lists, roff);
-  note_launch();
-  return check_launch("cm_lists");
+  char* base = static_cast<char*>(lists_ws);
+  for (int64_t b0 = 0; b0 < m; b0 += cap) {
+    const int nb = (int)std::min<int64_t>(cap, m - b0);
+    uint32_t* words = reinterpret_cast<uint32_t*>(base);
+    int32_t* hdr = reinterpret_cast<int32_t*>(base + align_up(sizeof(uint32_t) * (size_t)ntiles * plan_tile_words(s)));
+    const size_t smem = plan_smem_bytes(s, nb);
+    int rc = set_smem(cm_plan_kernel, smem);
+    if (rc) return rc;
+    cm_plan_kernel<<<(unsigned)ntiles, 256, smem, st>>>(col_rows, col_signs, s, K2, lo, nvalid, (int)b0, nb, words,
+                                                         hdr);
+    note_launch();
+    if ((rc = check_launch("cm_plan"))) return rc;
+    base += plan_range_bytes(ntiles, s);
+  }
+  return SKH_OK;
 }
 
-// Final pass: bits [lo, lo + K2) then gather into SA columns (buckets in
-// ranges of at most cm_max_buckets(s), one launch per range).
+// Final pass: bits [lo, lo + K2) then the owner-planned gather into SA columns
+// (one launch per bucket range).
 int launch_cm_gather(const double* X, int64_t ldx, int64_t ncolX, const double* xb, int64_t nvalid, int64_t ntiles,
                      int lo, int K2, const void* lists_ws, int s, int64_t m, double* SA, int64_t ldsa,
                      int64_t ncolSA, double* Sb, double alpha, cudaStream_t st) {
@@ -1025,9 +853,6 @@ int launch_cm_gather(const double* X, int64_t ldx, int64_t ncolX, const double* 
   a.nvalid = nvalid;
   a.ntiles = ntiles;
   a.lo = lo;
-  a.lists = static_cast<const uint32_t*>(lists_ws);
-  a.roff = reinterpret_cast<const int32_t*>(static_cast<const char*>(lists_ws) +
-                                            align_up(sizeof(uint32_t) * (size_t)ntiles * list_cap(s)));
   a.s = s;
   a.SA = SA;
   a.ldsa = ldsa;
@@ -1039,23 +864,27 @@ int launch_cm_gather(const double* X, int64_t ldx, int64_t ncolX, const double* 
     set_error("column-major gather supports s <= 8");
     return SKH_EINVAL;
   }
+  const char* base = static_cast<const char*>(lists_ws);
   for (int64_t b0 = 0; b0 < m; b0 += cap) {
     a.b0 = (int)b0;
     a.nb = (int)std::min<int64_t>(cap, m - b0);
+    a.words = reinterpret_cast<const uint32_t*>(base);
+    a.hdr = reinterpret_cast<const int32_t*>(base + align_up(sizeof(uint32_t) * (size_t)ntiles * plan_tile_words(s)));
     int rc;
     switch (K2) {
-      case 0: rc = launch_pass2_t<0, true>(a, st); break;
-      case 1: rc = launch_pass2_t<1, true>(a, st); break;
-      case 2: rc = launch_pass2_t<2, true>(a, st); break;
-      case 3: rc = launch_pass2_t<3, true>(a, st); break;
-      case 4: rc = launch_pass2_t<4, true>(a, st); break;
-      case 5: rc = launch_pass2_t<5, true>(a, st); break;
-      case 6: rc = launch_pass2_t<6, true>(a, st); break;
-      case 7: rc = launch_pass2_t<7, true>(a, st); break;
-      case 8: rc = launch_pass2_t<8, true>(a, st); break;
+      case 0: rc = launch_gather_t<0>(a, st); break;
+      case 1: rc = launch_gather_t<1>(a, st); break;
+      case 2: rc = launch_gather_t<2>(a, st); break;
+      case 3: rc = launch_gather_t<3>(a, st); break;
+      case 4: rc = launch_gather_t<4>(a, st); break;
+      case 5: rc = launch_gather_t<5>(a, st); break;
+      case 6: rc = launch_gather_t<6>(a, st); break;
+      case 7: rc = launch_gather_t<7>(a, st); break;
+      case 8: rc = launch_gather_t<8>(a, st); break;
       default: set_error("cm gather: K2 = %d", K2); return SKH_EINVAL;
     }
     if (rc) return rc;
+    base += plan_range_bytes(ntiles, s);
   }
   return SKH_OK;
 }

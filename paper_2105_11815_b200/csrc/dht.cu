@@ -28,7 +28,7 @@
 namespace skh {
 
 // cm.cu
-size_t cm_lists_bytes(int64_t ntiles, int s);
+size_t cm_lists_bytes(int64_t ntiles, int s, int64_t m);
 int launch_cm_lists(const int32_t* col_rows, const int8_t* col_signs, int s, int64_t m, int K2, int lo,
                     int64_t nvalid, int64_t ntiles, void* lists_ws, cudaStream_t st);
 int launch_cm_gather(const double* X, int64_t ldx, int64_t ncolX, const double* xb, int64_t nvalid, int64_t ntiles,
@@ -265,7 +265,7 @@ DhtWs dht_layout(void* base, int64_t n, int64_t m, int s, int64_t d, bool rowmaj
   w.rows = (int32_t*)take(sizeof(int32_t) * (size_t)n * s);
   w.signs = (int8_t*)take((size_t)n * s);
   w.hws = take(hash_ws_bytes(n, m, s));
-  if (!rowmajor && !pow2) w.lists = take(cm_lists_bytes((n + 4095) / 4096, s));
+  if (!rowmajor && !pow2) w.lists = take(cm_lists_bytes((n + 4095) / 4096, s, m));
   w.total = off;
   return w;
 }

@@ -14,7 +14,6 @@
 // flip; its bits come from a per-call bitmap of the splitmix64 words
 // u(key_DIAG, g >> 6), loaded before the data so the 16 data loads stay in
 // flight together.  Zero padding rows are never read.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -24,27 +23,11 @@
 
 #include "common.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace skh {
 namespace {
 
 constexpr int kGenThreads = 256;
 
-int wide_mode();
-
-}  // namespace
-
-// fwht_fused.cu
-int launch_fused2_k(int K, bool diag, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo,
-                    int64_t d, int64_t g_begin, int64_t g_count, uint32_t* counters, uint64_t dkey, int64_t row0,
-                    double alpha, cudaStream_t st);
-// fwht_pipe.cu
-int launch_pipe_k(int K, bool diag, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo,
-                  int64_t d, int64_t g_begin, int64_t g_count, uint32_t* counters, uint64_t dkey, int64_t row0,
-                  double alpha, cudaStream_t st);
-
-namespace {
 
 __global__ void diag_words_kernel(uint64_t key, int64_t w0, int64_t nw, uint64_t* __restrict__ out) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -191,265 +174,6 @@ __global__ void __launch_bounds__(tile_threads<K>()) fwht_tile_kernel(
   }
 }
 
-// Cluster pass: K = KL + CB bits on a thread-block cluster of C = 2^CB CTAs.
-// CTA q holds the rows whose top CB mid bits equal q (2^KL rows x TC columns,
-// 64 KiB); it runs the KL local bits exactly like fwht_tile_kernel, then one
-// all-to-all through distributed shared memory (remote st.shared::cluster)
-// gives every CTA all C values of the top bits for 2^KL / C of the low mids,
-// and the CB cross stages finish in registers.  HBM sees one read and one
-// write per element for all K bits, with 512 B (KL=7) row segments.
-template <int KL, int CB, bool DIAG>
-__global__ void __launch_bounds__(tile_threads<KL>()) fwht_cluster_kernel(
-    const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy, int64_t nvalid, int lo,
-    int64_t d, int64_t ntc, int64_t g_begin, uint64_t dkey, int64_t row0, double alpha) {
-  constexpr int K = KL + CB;
-  constexpr int C = 1 << CB;
-  constexpr int TC = tile_cols<KL>();
-  constexpr int CP = TC / 2;
-  constexpr int NPH = (KL + 3) / 4;
-  constexpr int ML = 1 << KL;
-  constexpr int MP = ML / C;  // low-mid values owned by each CTA in the cross phase
-  constexpr int NT = 16 / C;  // low-mid values per thread in the cross phase
-  extern __shared__ double2 tile[];  // [2^KL][CP]
-  cg::cluster_group cluster = cg::this_cluster();
-  const int q = (int)cluster.block_rank();
-  const int cp = threadIdx.x % CP, rs = threadIdx.x / CP;
-  const int64_t cid = blockIdx.x / C;
-  const int64_t g = g_begin + cid / ntc;
-  const int64_t tc = cid % ntc;
-  const int64_t low = g & (((int64_t)1 << lo) - 1);
-  const int64_t hi = g >> lo;
-  const int64_t rbase = (hi << (lo + K)) + low;
-  const int64_t c = tc * TC + 2 * cp;
-  const bool cv = c < d;
-
-  uint32_t negmask = 0;
-  if (DIAG) {
-    if (lo == 0) {
-      const int64_t g0 = row0 + rbase + q * ML + mid_of<KL, 0>(rs, 0);
-      const uint64_t wa = stream_u(dkey, (uint64_t)(g0 >> 6)), wb = stream_u(dkey, (uint64_t)((g0 + 15) >> 6));
-#pragma unroll
-      for (int v = 0; v < 16; ++v) {
-        const int64_t gr = g0 + v;
-        const uint64_t w = ((gr >> 6) == (g0 >> 6)) ? wa : wb;
-        if (gr - row0 < nvalid) negmask |= (uint32_t)((w >> (gr & 63)) & 1ull) << v;
-      }
-    } else {
-#pragma unroll
-      for (int v = 0; v < 16; ++v) {
-        const int64_t r = rbase + ((int64_t)(q * ML + mid_of<KL, 0>(rs, v)) << lo);
-        const int64_t gr = row0 + r;
-        if (r < nvalid) negmask |= (uint32_t)((stream_u(dkey, (uint64_t)(gr >> 6)) >> (gr & 63)) & 1ull) << v;
-      }
-    }
-  }
-  double2 x[16];
-#pragma unroll
-  for (int v = 0; v < 16; ++v) {
-    const int64_t r = rbase + ((int64_t)(q * ML + mid_of<KL, 0>(rs, v)) << lo);
-    x[v] = (cv && r < nvalid) ? __ldg(reinterpret_cast<const double2*>(X + r * ldx + c)) : make_double2(0.0, 0.0);
-  }
-  if (DIAG) {
-#pragma unroll
-    for (int v = 0; v < 16; ++v)
-      if ((negmask >> v) & 1u) x[v] = make_double2(-x[v].x, -x[v].y);
-  }
-  phase_stages<KL, 0>(x);
-  if constexpr (NPH > 1) {
-    exchange<KL, 0, CP>(x, tile, cp, rs);
-    phase_stages<KL, 1>(x);
-  }
-  if constexpr (NPH > 2) {
-    exchange<KL, 1, CP>(x, tile, cp, rs);
-    phase_stages<KL, 2>(x);
-  }
-  // cross-CTA all-to-all: value for low-mid m goes to CTA m / MP, slot (m % MP) * C + q
-  cluster.sync();  // every CTA has finished reading its own tile buffer
-#pragma unroll
-  for (int v = 0; v < 16; ++v) {
-    const int m = mid_of<KL, NPH - 1>(rs, v);
-    double2* dst = cluster.map_shared_rank(tile, m / MP);
-    dst[((m % MP) * C + q) * CP + cp] = x[v];
-  }
-  cluster.sync();  // all remote stores landed
-#pragma unroll
-  for (int t = 0; t < NT; ++t)
-#pragma unroll
-    for (int qq = 0; qq < C; ++qq) x[t * C + qq] = tile[((rs * NT + t) * C + qq) * CP + cp];
-#pragma unroll
-  for (int bb = 0; bb < CB; ++bb) {
-    const int h = 1 << bb;
-#pragma unroll
-    for (int t = 0; t < NT; ++t)
-#pragma unroll
-      for (int qq = 0; qq < C; ++qq)
-        if (!(qq & h)) {
-          const double2 a = x[t * C + qq], b = x[t * C + qq + h];
-          x[t * C + qq] = add2(a, b);
-          x[t * C + qq + h] = sub2(a, b);
-        }
-  }
-  if (cv) {
-#pragma unroll
-    for (int t = 0; t < NT; ++t)
-#pragma unroll
-      for (int qq = 0; qq < C; ++qq) {
-        const int mid = qq * ML + q * MP + rs * NT + t;
-        const int64_t r = rbase + ((int64_t)mid << lo);
-        const double2 v = x[t * C + qq];
-        *reinterpret_cast<double2*>(Y + r * ldy + c) = make_double2(alpha * v.x, alpha * v.y);
-      }
-  }
-}
-
-// Fused pass through L2: K = 7 + KB bits with one HBM read and one HBM write.
-// A unit (group of 2^K rows x 64 columns, 2^K * 512 B) is split into 2^KB
-// A-tasks (a 7-bit tile over the low mid bits, exactly fwht_tile_kernel<7>) and
-// 2^KB B-tasks (the KB high mid bits for 128 / 2^KB low-mid values, all in
-// registers).  A persistent grid pulls tasks from an atomic counter in an
-// order that interleaves A-tasks of unit u with B-tasks of unit u - LAG; a
-// B-task waits (acquire) until the unit's A-tasks have published (release)
-// their stores, then reads them with ld.global.cg -- from L2, where they still
-// are because only ~LAG units (tens of MiB) are in flight.  B-tasks never block
-// A-tasks and tasks are claimed in dependency order, so the schedule cannot
-// deadlock whatever the residency.  Stage order stays low bit -> high bit.
-template <int KB, bool DIAG>
-__global__ void __launch_bounds__(256, 3) fwht_fused_kernel(
-    const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy, int64_t nvalid, int lo,
-    int64_t d, int64_t ntc, int64_t g_begin, int64_t nunits, int64_t lag, uint32_t* __restrict__ counters,
-    uint64_t dkey, int64_t row0, double alpha) {
-  constexpr int K = 7 + KB;
-  constexpr int TC = 64, CP = 32;
-  constexpr int NB = 1 << KB;       // A-tasks (and B-tasks) per unit
-  constexpr int NA = 16 / NB;       // low-mid values per thread in a B-task
-  extern __shared__ double2 tile[];  // [128][CP]
-  __shared__ int64_t s_task;
-  uint32_t* task_ctr = counters;
-  uint32_t* done = counters + 64;
-  const int cp = threadIdx.x % CP, rs = threadIdx.x / CP;
-  const int64_t lagc = lag < nunits ? lag : nunits;
-  const int64_t nblocks = 2 * nunits;
-  for (;;) {
-    if (threadIdx.x == 0) s_task = (int64_t)atomicAdd(task_ctr, 1u);
-    __syncthreads();
-    const int64_t t = s_task;
-    __syncthreads();
-    if (t >= nblocks * NB) break;
-    // decode: block k = t / NB; blocks A_0..A_{lag-1}, then (A_{lag+i}, B_i) pairs, then the last B's
-    const int64_t k = t / NB;
-    const int sub = (int)(t % NB);
-    int64_t u;
-    bool isA;
-    if (k < lagc) {
-      u = k;
-      isA = true;
-    } else if (k < lagc + 2 * (nunits - lagc)) {
-      const int64_t j = k - lagc;
-      isA = (j & 1) == 0;
-      u = isA ? lagc + j / 2 : j / 2;
-    } else {
-      isA = false;
-      u = (nunits - lagc) + (k - lagc - 2 * (nunits - lagc));
-    }
-    const int64_t g = g_begin + u / ntc;
-    const int64_t tc = u % ntc;
-    const int64_t low = g & (((int64_t)1 << lo) - 1);
-    const int64_t hi = g >> lo;
-    const int64_t rbase = (hi << (lo + K)) + low;
-    const int64_t c = tc * TC + 2 * cp;
-    const bool cv = c < d;
-    double2 x[16];
-    if (isA) {
-      // rows mid = a + 128 * sub, a = 0..127 (a 7-bit tile)
-      const int64_t rb = rbase + ((int64_t)(sub * 128) << lo);
-      uint32_t negmask = 0;
-      if (DIAG) {
-        if (lo == 0) {
-          const int64_t g0 = row0 + rb + mid_of<7, 0>(rs, 0);
-          const uint64_t wa = stream_u(dkey, (uint64_t)(g0 >> 6)), wb = stream_u(dkey, (uint64_t)((g0 + 15) >> 6));
-#pragma unroll
-          for (int v = 0; v < 16; ++v) {
-            const int64_t gr = g0 + v;
-            const uint64_t w = ((gr >> 6) == (g0 >> 6)) ? wa : wb;
-            if (gr - row0 < nvalid) negmask |= (uint32_t)((w >> (gr & 63)) & 1ull) << v;
-          }
-        } else {
-#pragma unroll
-          for (int v = 0; v < 16; ++v) {
-            const int64_t r = rb + ((int64_t)mid_of<7, 0>(rs, v) << lo);
-            const int64_t gr = row0 + r;
-            if (r < nvalid) negmask |= (uint32_t)((stream_u(dkey, (uint64_t)(gr >> 6)) >> (gr & 63)) & 1ull) << v;
-          }
-        }
-      }
-#pragma unroll
-      for (int v = 0; v < 16; ++v) {
-        const int64_t r = rb + ((int64_t)mid_of<7, 0>(rs, v) << lo);
-        x[v] = (cv && r < nvalid) ? __ldg(reinterpret_cast<const double2*>(X + r * ldx + c))
-                                  : make_double2(0.0, 0.0);
-      }
-      if (DIAG) {
-#pragma unroll
-        for (int v = 0; v < 16; ++v)
-          if ((negmask >> v) & 1u) x[v] = make_double2(-x[v].x, -x[v].y);
-      }
-      phase_stages<7, 0>(x);
-      exchange<7, 0, CP>(x, tile, cp, rs);
-      phase_stages<7, 1>(x);
-      if (cv) {
-#pragma unroll
-        for (int v = 0; v < 16; ++v) {
-          const int64_t r = rb + ((int64_t)mid_of<7, 1>(rs, v) << lo);
-          *reinterpret_cast<double2*>(Y + r * ldy + c) = x[v];
-        }
-      }
-      // publish: CTA barrier, then one gpu-scope release (cumulative over the
-      // CTA's stores ordered before it by the barrier)
-      __syncthreads();
-      if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(done + u) : "memory");
-    } else {
-      if (threadIdx.x == 0) {
-        unsigned ns = 32;
-        for (;;) {
-          uint32_t v;
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done + u) : "memory");
-          if (v >= (uint32_t)NB) break;
-          __nanosleep(ns);
-          if (ns < 1024) ns *= 2;
-        }
-      }
-      __syncthreads();
-      // value v = aa * NB + b: low mid a = sub * (128 / NB) + rs * NA + aa, high bits b
-#pragma unroll
-      for (int v = 0; v < 16; ++v) {
-        const int aa = v / NB, b = v % NB;
-        const int mid = sub * (128 / NB) + rs * NA + aa + 128 * b;
-        const int64_t r = rbase + ((int64_t)mid << lo);
-        x[v] = cv ? __ldcg(reinterpret_cast<const double2*>(Y + r * ldy + c)) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int bb = 0; bb < KB; ++bb) {
-        const int h = 1 << bb;
-#pragma unroll
-        for (int v = 0; v < 16; ++v)
-          if (!(v & h)) {
-            const double2 a = x[v], b = x[v + h];
-            x[v] = add2(a, b);
-            x[v + h] = sub2(a, b);
-          }
-      }
-      if (cv) {
-#pragma unroll
-        for (int v = 0; v < 16; ++v) {
-          const int aa = v / NB, b = v % NB;
-          const int mid = sub * (128 / NB) + rs * NA + aa + 128 * b;
-          const int64_t r = rbase + ((int64_t)mid << lo);
-          *reinterpret_cast<double2*>(Y + r * ldy + c) = make_double2(alpha * x[v].x, alpha * x[v].y);
-        }
-      }
-    }
-  }
-}
 
 // Generic pass: any d, any alignment, K in [0, 5]; one thread per (group, column).
 template <int K>
@@ -515,113 +239,6 @@ int launch_tile(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nv
   return check_launch("fwht_tile");
 }
 
-template <int KL, int CB, bool DIAG>
-int launch_cluster(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo, int64_t d,
-                   int64_t g_begin, int64_t g_count, uint64_t dkey, int64_t row0, double alpha, cudaStream_t st) {
-  constexpr int TC = tile_cols<KL>();
-  constexpr int T = tile_threads<KL>();
-  constexpr int C = 1 << CB;
-  const size_t smem = (size_t)(1 << KL) * TC * sizeof(double);
-  auto kern = fwht_cluster_kernel<KL, CB, DIAG>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  const int64_t ntc = (d + TC - 1) / TC;
-  const int64_t max_groups = ((1ll << 31) - 1) / (ntc * C);
-  for (int64_t g0 = g_begin; g0 < g_begin + g_count; g0 += max_groups) {
-    const int64_t gc = std::min(max_groups, g_begin + g_count - g0);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(gc * ntc * C), 1, 1);
-    cfg.blockDim = dim3(T, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, X, ldx, Y, ldy, nvalid, lo, d, ntc, g0, dkey, row0, alpha);
-    note_launch();
-    if (e != cudaSuccess) {
-      set_error("fwht_cluster launch: %s", cudaGetErrorString(e));
-      return SKH_ECUDA;
-    }
-  }
-  return check_launch("fwht_cluster");
-}
-
-// K in [9, 11]: local bits KL (TC = 64 for KL = 7, 32 for KL = 8) + CB cross bits.
-int launch_cluster_k(int K, bool diag, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo,
-                     int64_t d, int64_t g_begin, int64_t g_count, uint64_t dkey, int64_t row0, double alpha,
-                     cudaStream_t st) {
-#define SKH_CL(KL, CB)                                                                                               \
-  return diag ? launch_cluster<KL, CB, true>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dkey, row0, alpha, st) \
-              : launch_cluster<KL, CB, false>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dkey, row0, alpha, st)
-  switch (K) {
-    case 9: SKH_CL(7, 2);
-    case 10: SKH_CL(7, 3);
-    case 11: SKH_CL(8, 3);
-    default: break;
-  }
-#undef SKH_CL
-  set_error("internal: bad cluster pass width %d", K);
-  return SKH_EINVAL;
-}
-
-int sm_count() {
-  static int v = [] {
-    int dev = 0, n = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
-  }();
-  return v;
-}
-
-template <int KB, bool DIAG>
-int launch_fused(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo, int64_t d,
-                 int64_t g_begin, int64_t g_count, uint32_t* counters, uint64_t dkey, int64_t row0, double alpha,
-                 cudaStream_t st) {
-  constexpr int NB = 1 << KB;
-  const size_t smem = 128 * 32 * sizeof(double2);
-  auto kern = fwht_fused_kernel<KB, DIAG>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
-  if (per_sm < 1) per_sm = 1;
-  const int64_t resident = (int64_t)per_sm * sm_count();
-  const int64_t ntc = (d + 63) / 64;
-  const int64_t nunits = g_count * ntc;
-  const int64_t ntasks = 2 * nunits * NB;
-  const int64_t lag = std::max<int64_t>(1, (resident + 2 * NB - 1) / (2 * NB));
-  const int64_t grid = std::min<int64_t>(resident, ntasks);
-  cudaMemsetAsync(counters, 0, sizeof(uint32_t) * (size_t)(64 + nunits), st);
-  kern<<<(unsigned)grid, 256, smem, st>>>(X, ldx, Y, ldy, nvalid, lo, d, ntc, g_begin, nunits, lag, counters, dkey,
-                                           row0, alpha);
-  note_launch();
-  return check_launch("fwht_fused");
-}
-
-int launch_fused_k(int K, bool diag, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo,
-                   int64_t d, int64_t g_begin, int64_t g_count, uint32_t* counters, uint64_t dkey, int64_t row0,
-                   double alpha, cudaStream_t st) {
-#define SKH_FU(KB)                                                                                                 \
-  return diag ? launch_fused<KB, true>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0,      \
-                                       alpha, st)                                                                  \
-              : launch_fused<KB, false>(X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0,     \
-                                        alpha, st)
-  switch (K) {
-    case 9: SKH_FU(2);
-    case 10: SKH_FU(3);
-    case 11: SKH_FU(4);
-    default: break;
-  }
-#undef SKH_FU
-  set_error("internal: bad fused pass width %d", K);
-  return SKH_EINVAL;
-}
-
 template <int K>
 int launch_generic(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo, int64_t d,
                    int64_t g_begin, int64_t g_count, const uint64_t* dw, int64_t row0, int64_t w0, int apply_diag,
@@ -647,21 +264,12 @@ int launch_tile_d(bool diag, const double* X, int64_t ldx, double* Y, int64_t ld
 }
 
 int launch_pass(bool fast, int K, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t nvalid, int lo,
-                int64_t d, int64_t g_begin, int64_t g_count, const uint64_t* dw, uint32_t* counters, uint64_t dkey,
+                int64_t d, int64_t g_begin, int64_t g_count, const uint64_t* dw, uint64_t dkey,
                 int64_t row0, int64_t w0, int apply_diag, double alpha, cudaStream_t st) {
   const bool dg = apply_diag != 0;
   if (fast) {
 #define SKH_TILE(KK) \
   case KK: return launch_tile_d<KK>(dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dkey, row0, alpha, st)
-    if (K >= 7 && K <= 11 && wide_mode() == 3)
-      return launch_pipe_k(K, dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0, alpha, st);
-    if (K >= 8 && K <= 11 && wide_mode() == 4)
-      return launch_fused2_k(K, dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0, alpha,
-                             st);
-    if (K >= 9 && K <= 11 && wide_mode() == 1)
-      return launch_fused_k(K, dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, counters, dkey, row0, alpha, st);
-    if (K >= 9 && K <= 11 && wide_mode() == 2)
-      return launch_cluster_k(K, dg, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, dkey, row0, alpha, st);
     switch (K) {
       SKH_TILE(4);
       SKH_TILE(5);
@@ -701,23 +309,6 @@ int kmax_fast() {
     const char* e = getenv("SKH_FWHT_KMAX");
     int k = e ? atoi(e) : 10;
     return k < 4 ? 4 : (k > 11 ? 11 : k);
-  }();
-  return v;
-}
-
-// Kernel for passes wider than 8 bits (only used when SKH_FWHT_KMAX > 8):
-// 0 = single-CTA tiles (default), 1 = fused through L2, 2 = thread-block
-// clusters over DSMEM, 3 = bulk-copy pipeline (also takes 7- and 8-bit passes);
-// SKH_FWHT_WIDE = tile|fused|cluster|pipe.  Measurements: DESIGN.md §5.
-int wide_mode() {
-  static int v = [] {
-    const char* e = getenv("SKH_FWHT_WIDE");
-    if (!e) return 0;
-    if (e[0] == 'c') return 2;
-    if (e[0] == 'f') return 1;
-    if (e[0] == 'p') return 3;
-    if (e[0] == 's') return 4;  // "sched": cooperative static-schedule fused passes
-    return 0;  // "tile"
   }();
   return v;
 }
@@ -767,11 +358,8 @@ bool fwht_fast_ok(const double* X, int64_t ldx, const double* Y, int64_t ldy, in
          ldy % 2 == 0 && d % 2 == 0 && d >= 16;
 }
 
-// Workspace of a transform call: [task counter + per-unit counters of fused
-// passes][D bitmap for the generic first pass].
-size_t fwht_counter_bytes(int64_t nrows, int64_t d) {
-  return align_up(sizeof(uint32_t) * (size_t)(64 + std::max<int64_t>(1, (nrows >> 7) * ((d + 63) / 64))));
-}
+// Workspace of a transform call: [256-byte header][D bitmap for the generic first pass].
+size_t fwht_counter_bytes(int64_t, int64_t) { return 256; }
 
 size_t fwht_ws_bytes(int64_t nrows, int64_t nvalid, int64_t row0, int64_t d) {
   size_t b = fwht_counter_bytes(nrows, d);
@@ -801,8 +389,7 @@ int launch_fwht_pass_range(uint64_t seed, int K, bool fast, const double* X, int
                            int64_t nrows, int64_t nvalid, int lo, int64_t d, int64_t g_begin, int64_t g_count,
                            void* ws, int64_t row0, int apply_diag, double alpha, cudaStream_t st) {
   if (fast && (K < 4 || K > 11)) fast = false;
-  return launch_pass(fast, K, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, bitmap_of(ws, nrows, d),
-                     static_cast<uint32_t*>(ws), key_diag(seed), row0, row0 >> 6, apply_diag, alpha, st);
+  return launch_pass(fast, K, X, ldx, Y, ldy, nvalid, lo, d, g_begin, g_count, bitmap_of(ws, nrows, d), key_diag(seed), row0, row0 >> 6, apply_diag, alpha, st);
 }
 
 int launch_fwht(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, int64_t d, const double* X,
@@ -821,7 +408,7 @@ int launch_fwht(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0, int6
     const bool first = p == 0, last = p + 1 == ks.size();
     const int64_t ngroups = nrows >> K;
     rc = launch_pass(fast && K >= 4, K, first ? X : Y, first ? ldx : ldy, Y, ldy, first ? nvalid : nrows, lo, d, 0,
-                     ngroups, bitmap_of(ws, nrows, d), static_cast<uint32_t*>(ws), key_diag(seed), row0, row0 >> 6,
+                     ngroups, bitmap_of(ws, nrows, d), key_diag(seed), row0, row0 >> 6,
                      first ? apply_diag : 0, last ? alpha : 1.0, st);
     if (rc) return rc;
     lo += K;

@@ -101,9 +101,9 @@ def test_error_codes_widened_entry_points(lib):
     # variant: the same argument rules as skh_hash_gen
     assert lib.skh_hash_gen_variant(1, 4, 5, 10, 0, 0, 0, None, None, p, p, p, p, 1 << 20, None) == EINVAL
     assert lib.skh_hash_gen_variant(1, 8, 2, 10, 0, 0, 0, None, None, p, p, p, None, 0, None) == EWS
-    # column-major HRHT: s <= 8, m <= 65536, lda >= n, ldsa >= m, Sb with b, workspace
+    # column-major HRHT: s <= 8, lda >= n, ldsa >= m, Sb with b, workspace (any m: bucket ranges)
     assert lib.skh_rht_dense_colmajor(1, 100, 40, 9, 4, p, 100, None, p, 40, None, p, 1 << 30, None) == EINVAL
-    assert lib.skh_rht_dense_colmajor(1, 100, 70000, 1, 4, p, 100, None, p, 70000, None, p, 1 << 30, None) == EINVAL
+    assert lib.skh_rht_dense_colmajor(1, 100, 70000, 1, 4, p, 100, None, p, 70000, None, p, 64, None) == EWS
     assert lib.skh_rht_dense_colmajor(1, 100, 40, 1, 4, p, 99, None, p, 40, None, p, 1 << 30, None) == EDIM
     assert lib.skh_rht_dense_colmajor(1, 100, 40, 1, 4, p, 100, None, p, 39, None, p, 1 << 30, None) == EDIM
     assert lib.skh_rht_dense_colmajor(1, 100, 40, 1, 4, p, 100, p, p, 40, None, p, 1 << 30, None) == EDIM

@@ -188,7 +188,7 @@ def test_sketch_csr_C4_full_sampled_buckets():
     (4096, 4096, 64, 0, 12, True, 0), (4096, 3000, 64, 0, 12, True, 100), (1024, 1024, 32, 3, 9, False, 0),
     (2048, 2048, 18, 0, 11, True, 64), (1 << 16, 1 << 16, 16, 0, 16, True, 0), (512, 512, 130, 0, 9, True, 0),
     (8192, 8192, 2, 0, 13, True, 5),
-    # single cluster passes (K = 9, 10, 11 -> 4- and 8-CTA clusters), ragged column tiles, lo > 0, padding
+    # single wide tile passes (K = 9, 10, 11), ragged column tiles, lo > 0, padding
     (512, 512, 64, 0, 9, True, 0), (1024, 1024, 70, 0, 10, True, 3), (2048, 2000, 64, 0, 11, True, 0),
     (4096, 4096, 96, 1, 11, False, 0), (8192, 8192, 32, 2, 13, True, 1 << 20), (1 << 12, 3333, 200, 0, 11, True, 64)])
 def test_rht_stages(nrows, nvalid, d, lo, hi, diag, row0):
