@@ -224,92 +224,140 @@ def e2e_measure(cfg, inputs, steps, torch, layout="row"):
                     "skh_rht_dense_host" if cfg.hd else "skh_sketch_dense_host")}
 
 
-def roofline(cfg, step, stage_ms, peak_gbs, peak_src, layout="row", sketch="hashing"):
-    """Dominant kernel and its algorithmic bytes per launch."""
+SPEC_HBM_GBS = 8000.0  # B200 HBM3e spec sheet: the secondary denominator
+
+
+def alg_bytes_step(cfg, n_hash):
+    """SURVEY §8(d) algorithmic bytes of one whole step: read A (dense n d 8, or
+    the CSR arrays) and b once, write SA and Sb once, plus s 5 bytes of bucket
+    metadata (int32 row + int8 sign) per hashed row.  H D adds adds, not bytes."""
+    return cfg.a_bytes + cfg.n * 8 + cfg.m * cfg.d * 8 + cfg.m * 8 + n_hash * cfg.s * 5
+
+
+def kernel_table(cfg, step, layout, sketch):
+    """Stage name -> (kernel, algorithmic bytes per launch, launches per step):
+    per §8(d), a launch that reads X rows of A costs X d 8 bytes (a transform
+    pass included: a fused transform would add none), a gather also writes SA
+    and reads its bucket metadata."""
     if sketch in ("dht", "srdht"):
-        # stages of skh_hrdht_dense / skh_srdht_dense (row-major).  n = 2^L
-        # (csrc/fht.cu): pass A reads D [A | b] and writes the half spectrum
-        # (n/2 + n1 complex per column ~ the same bytes), pass B reads it and
-        # writes the row-major transform.  Other n (or SKH_DHT_CUFFT=1): D +
-        # transpose, cuFFT D2Z (a library FFT), Hartley combine + transpose.
-        # Then the gather (or row sampling) reads the transform once.
         nb = cfg.n * (cfg.d + 1) * 8
-        alg = {"diag": 2 * nb, "fft": 2 * nb, "hartley": 2 * nb, "dht_passA": 2 * nb, "dht_passB": 2 * nb,
-               "gather": nb + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5}
-        name = max((k for k in stage_ms if k in alg), key=lambda k: stage_ms[k])
-        t = stage_ms[name]
-        ach = alg[name] / (t / 1e3) / 1e9
-        return {"bound": "hbm", "kernel": ("cufft D2Z (library)" if name == "fft" else name), "achieved": round(ach, 1),
-                "peak": peak_gbs, "unit": "GB/s", "frac": round(ach / peak_gbs, 4), "traffic": None,
-                "traffic_source": None, "alg_bytes_per_launch": alg[name], "ms_per_launch": round(t, 4),
-                "peak_source": peak_src}
-    if layout == "col" and "transpose" in stage_ms:
-        # plain column-major sketch with the transposed path (skh.h): the tiled
-        # transpose reads + writes A once; the row gather reads the copy once,
-        # writes SA, and SA is transposed out (read + write)
-        nb = cfg.n * cfg.d * 8
-        alg = {"transpose": 2 * nb, "gather": nb + 3 * cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5}
-        label = {"transpose": "cm_to_rm_kernel (A transpose)", "gather": "gather_wide + SA transpose"}
-        name = max((k for k in stage_ms if k in alg), key=lambda k: stage_ms[k])
-        t = stage_ms[name]
-        achieved = alg[name] / (t / 1e3) / 1e9
-        return {"bound": "hbm", "kernel": label[name], "achieved": round(achieved, 1), "peak": peak_gbs,
-                "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": None, "traffic_source": None,
-                "alg_bytes_per_launch": alg[name], "ms_per_launch": round(t, 4), "peak_source": peak_src}
-    if layout == "col":
-        # dominant by time; algorithmic bytes of each kernel per launch:
-        #  pass1: read + write (d + 1) columns of n_pad rows once
-        #  pass2_gather / gather: read the columns once, write SA, read the tile lists
+        return {"dht_passA": ("dht_passA_kernel", nb, 1), "dht_passB": ("dht_passB_kernel", nb, 1),
+                "diag": ("diag_transpose", nb, 1), "fft": ("cufft D2Z (library)", nb, 1),
+                "hartley": ("hartley combine", nb, 1),
+                "gather": ("gather", nb + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5, 1)}
+    if layout == "col" and cfg.kind != "csr":
         cols = cfg.d + 1
-        nrows = step.n_pad if cfg.hd else cfg.n
-        lists = nrows * cfg.s * 4
-        alg = {"pass1": 2 * step.n_pad * cols * 8,
-               "pass2_gather": nrows * cols * 8 + cfg.m * cols * 8 + lists,
-               "gather": nrows * cols * 8 + cfg.m * cols * 8 + lists}
-        name = max((k for k in stage_ms if k in alg), key=lambda k: stage_ms[k])
-        t = stage_ms[name]
-        achieved = alg[name] / (t / 1e3) / 1e9
-        traffic, tsrc = None, None
-        tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            with open(tp) as f:
-                ent = json.load(f).get(cfg.name + "-col")
-            if ent and ent["kernel"] == "cm_" + name:
-                traffic, tsrc = ent["dram_bytes_per_launch"], ent["source"]
-        return {"bound": "hbm", "kernel": "cm_" + name, "achieved": round(achieved, 1), "peak": peak_gbs,
-                "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": traffic, "traffic_source": tsrc,
-                "alg_bytes_per_launch": alg[name], "ms_per_launch": round(t, 4), "peak_source": peak_src,
-                "note": "bound on chip: the rank-round scatter into shared memory (DESIGN.md §5b); DRAM traffic "
-                        "equals the algorithmic bytes"}
+        if not cfg.hd:
+            nb = cfg.n * cfg.d * 8
+            return {"transpose": ("cm_to_rm_kernel (A transpose)", nb, 1),
+                    "gather": ("gather_wide + SA transpose", nb + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5, 1)}
+        npad = step.n_pad
+        return {"pass1": ("cm_pass1_kernel", npad * cols * 8, 1),
+                "mid_pass": ("cm_mid_kernel", npad * cols * 8, 1),
+                "pass2_gather": ("cm_gather_kernel (fused last pass + owner-planned gather)",
+                                 npad * cols * 8 + cfg.m * cols * 8 + npad * cfg.s * 5, 1)}
     if cfg.kind == "csr":
-        name = "gather_csr"
-        nnz = cfg.n * cfg.nnz_row
-        alg = nnz * 12 + (cfg.n + 1) * 8 + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5
-        t = stage_ms[name]
-    elif cfg.hd:
-        passes = [k for k in stage_ms if k.startswith("fwht_pass")]
-        name = "fwht_tile_kernel (" + "+".join(str(k) for k in step.plan) + " stage passes, mean per launch)"
-        alg = 2 * step.n_pad * cfg.d * 8          # read + write the n x d block once per pass
-        t = sum(stage_ms[k] for k in passes) / len(passes)
-    else:
-        name = "gather_wide" if (cfg.d % 2 == 0 and cfg.d > 64) else "gather_dense"  # csrc/gather.cu kernel
-        alg = cfg.n * cfg.d * 8 + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5
-        t = stage_ms["gather"]
-    achieved = alg / (t / 1e3) / 1e9
-    traffic, tsrc = None, None
+        return {"gather_csr": ("csr_expand + csr_reduce", cfg.a_bytes + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5, 1)}
+    if cfg.hd:
+        t = {f"fwht_pass{p}": (f"fwht_tile_kernel<{k}>", step.n_pad * cfg.d * 8, 1) for p, k in enumerate(step.plan)}
+        t["gather"] = ("gather_wide_kernel", step.n_pad * cfg.d * 8 + cfg.m * cfg.d * 8 + step.n_pad * cfg.s * 5, 1)
+        return t
+    name = "gather_wide_kernel" if (cfg.d % 2 == 0 and cfg.d > 64) else "gather_dense_kernel"
+    return {"gather": (name, cfg.n * cfg.d * 8 + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5, 1)}
+
+
+def traffic_record(cfg, layout):
+    """ncu DRAM bytes (read + write) per launch of each kernel of this workload's
+    step, from profiles/traffic.json (written from a committed launch list)."""
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            ent = json.load(f).get(cfg.name)
-        if ent and ent["kernel"].split("<")[0] in name:
-            traffic, tsrc = ent["dram_bytes_per_launch"], ent["source"]
-    out = {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": peak_gbs, "unit": "GB/s",
-           "frac": round(achieved / peak_gbs, 4), "traffic": traffic, "traffic_source": tsrc,
-           "alg_bytes_per_launch": alg, "ms_per_launch": round(t, 4), "peak_source": peak_src}
-    if achieved > peak_gbs:
-        out["note"] = ("frac > 1: the peak is torch's device copy (b.copy_ of 2 GiB, best of 10); this pass "
-                       "moves the same read + write bytes slightly faster")
+    if not os.path.exists(tp):
+        return None
+    with open(tp) as f:
+        return json.load(f).get(f"{cfg.name}-{layout}")
+
+
+def roofline(cfg, step, stage_ms, ms_step, peak_gbs, peak_src, layout="row", sketch="hashing"):
+    """The dominant kernel against the HBM roofline, and the whole step's
+    algorithmic-byte fraction, against the measured copy peak and
+    the 8 TB/s spec."""
+    table = kernel_table(cfg, step, layout, sketch)
+    n_hash = getattr(step, "n_pad", cfg.n) if cfg.hd else cfg.n
+    alg_step = alg_bytes_step(cfg, n_hash)
+    present = {k: v for k, v in stage_ms.items() if k in table}
+    name = max(present, key=lambda k: present[k])
+    kern, alg, nl = table[name]
+    t_launch = present[name] / nl
+    achieved = alg / (t_launch / 1e3) / 1e9
+    rec = traffic_record(cfg, layout)
+    traffic = None
+    step_traffic = None
+    if rec:
+        kt = rec.get("kernels", {})
+        if name in kt:
+            traffic = kt[name]["dram_bytes_per_launch"]
+        if all(k in kt for k in present):
+            step_traffic = sum(kt[k]["dram_bytes_per_launch"] * table[k][2] for k in present)
+    ach_step = alg_step / (ms_step / 1e3) / 1e9
+    out = {"bound": "hbm", "kernel": kern, "stage": name, "achieved": round(achieved, 1), "peak": peak_gbs,
+           "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": traffic,
+           "alg_bytes_per_launch": alg, "ms_per_launch": round(t_launch, 4), "peak_source": peak_src,
+           "frac_of_8tbs_spec": round(achieved / SPEC_HBM_GBS, 4),
+           "dram_frac": (round(traffic / (t_launch / 1e3) / 1e9 / peak_gbs, 4) if traffic else None),
+           "traffic_ratio": (round(traffic / alg, 3) if traffic else None),
+           "traffic_source": rec.get("source") if rec else None,
+           "step": {"alg_bytes": alg_step, "achieved": round(ach_step, 1), "alg_frac": round(ach_step / peak_gbs, 4),
+                    "alg_frac_of_8tbs_spec": round(ach_step / SPEC_HBM_GBS, 4), "traffic": step_traffic,
+                    "traffic_ratio": (round(step_traffic / alg_step, 3) if step_traffic else None),
+                    "note": "SURVEY §8(d): |A| + |b| + |SA| + |Sb| + s*5 B of lists per hashed row, over the "
+                            "step time"}}
     return out
+
+
+def default_layout(cfg):
+    """Storage of dense A the bench times by default: column-major (the paper's
+    LAPACK/FFTW layout) for an H D workload whose row-major transform
+    needs >= 3 HBM passes -- there the two-pass column-major plan (pass 2 fused
+    with the sketch) moves 3|A| instead of 7|A| and wins (C5) -- else
+    row-major (C2, C3HD: two row passes; plain sketches: one read)."""
+    if not cfg.hd or cfg.kind == "csr":
+        return "row"
+    from paper_2105_11815_b200 import api
+    n_pad = 1 << max(0, (cfg.n - 1).bit_length())
+    return "col" if len(api.rht_pass_plan(n_pad.bit_length() - 1, cfg.d)) >= 3 else "row"
+
+
+def freivalds_check(cfg, SA, inputs, layout, nprobe=4):
+    """Oracle-side whole-matrix check of the timed step's SA (SURVEY §8(c) tier
+    2): w^T (S A) v vs (S^T w)^T (A v) with S^T w from the oracle's column lists
+    (oracle/probes.py) and A v an fp64 library product of the input; bound
+    1e-12 ||w|| ||SA||_F ||v||."""
+    import numpy as np
+    import torch
+
+    from oracle import probes
+    SA = SA.detach().cpu().numpy()
+    if layout == "col" and cfg.kind != "csr":
+        SA = SA.T
+    if cfg.kind == "csr":
+        import scipy.sparse as sp
+
+        from synth import gen
+        rp, ci, v = gen.csr(cfg)
+        A = sp.csr_matrix((v, ci, rp), shape=(cfg.n, cfg.d))
+        Av_of = lambda x: A @ x  # noqa: E731
+    else:
+        X = inputs[0]
+        M = X.t() if layout == "col" else X
+        Av_of = lambda x: torch.mv(M, torch.from_numpy(x).to(M.device)).cpu().numpy()  # noqa: E731
+    rng = np.random.default_rng(2105)
+    worst = 0.0
+    for _ in range(nprobe):
+        w, v = rng.standard_normal(cfg.m), rng.standard_normal(cfg.d)
+        lhs = float(w @ (SA @ v))
+        rhs = (probes.probe_rht if cfg.hd else probes.probe_dense)(cfg.seed, cfg.n, cfg.m, cfg.s, w, Av_of(v))
+        worst = max(worst, abs(lhs - rhs) / (np.linalg.norm(w) * np.linalg.norm(SA) * np.linalg.norm(v)))
+    return {"ok": bool(worst <= 1e-12), "worst_rel": worst, "probes": nprobe, "bound": 1e-12,
+            "what": "w^T(SA)v vs (S^T w)^T(Av): all m x d entries of SA, oracle column lists"}
 
 
 def gpu_arm_single(args, cfg):
@@ -353,28 +401,37 @@ def gpu_arm_single(args, cfg):
                        "parallelism": "single GPU", "note": cfg.note},
             "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
             "gpu_launches": int(launches), "clocks": clocks}
-    line["roofline"] = roofline(cfg, step, stage_ms, pk["hbm_gbs"], src, args.layout, args.sketch)
+    line["roofline"] = roofline(cfg, step, stage_ms, ms, pk["hbm_gbs"], src, args.layout, args.sketch)
+    line["alg_frac"] = line["roofline"]["step"]["alg_frac"]
+    SA_last = step.run()[0] if not args.no_cpu_baseline else None
+    torch.cuda.synchronize()
     if args.sketch != "hashing":
         line["config"]["sketch"] = {"variant": "s-hashing variant (Def. 7)", "dht": "HR-DHT S_h F D (eq. (6.1))",
                                     "srdht": "SR-DHT S_s F D (eq. (7.2))"}[args.sketch]
-    del step
+    if SA_last is not None and args.sketch == "hashing":
+        # the oracle leg: a whole-matrix Freivalds check of the timed object's SA
+        fv = freivalds_check(cfg, SA_last, inputs, args.layout)
+        line["freivalds_ok"] = fv["ok"]
+        cpu_line = dict(cpu_line or {}, freivalds=fv)
+    del step, SA_last
     if not args.no_e2e:
         line["e2e"] = e2e_measure(cfg, inputs, args.e2e_steps, torch, args.layout) if args.sketch == "hashing" else None
     del inputs
     torch.cuda.empty_cache()
-    if args.layout == "row" and cfg.kind != "csr" and cfg.hd and args.sketch == "hashing" and not args.no_alt_layout:
-        line["column_major"] = alt_layout_measure(args, cfg, torch, pk, src)
+    if cfg.kind != "csr" and cfg.hd and args.sketch == "hashing" and not args.no_alt_layout:
+        alt = "row" if args.layout == "col" else "col"
+        line["row_major" if alt == "row" else "column_major"] = alt_layout_measure(args, cfg, torch, pk, src, alt)
         torch.cuda.empty_cache()
     if cpu_line is not None:
         line["cpu_baseline"] = cpu_line
     print(json.dumps(line), flush=True)
 
 
-def alt_layout_measure(args, cfg, torch, pk, src):
-    """The same workload stored column-major (the paper's LAPACK layout): the
-    two-pass fused path of skh_rht_dense_colmajor, timed the
-    same way; reported beside the row-major headline."""
-    step, inputs = build_step(cfg, torch, "col")
+def alt_layout_measure(args, cfg, torch, pk, src, layout):
+    """The same workload stored in the other layout, timed the same way and
+    reported beside the headline (column-major: skh_rht_dense_colmajor's two
+    passes; row-major: the tile passes + gather, §5)."""
+    step, inputs = build_step(cfg, torch, layout)
     torch.cuda.synchronize()
     for _ in range(max(args.warmup, 0)):
         step.run()
@@ -391,9 +448,11 @@ def alt_layout_measure(args, cfg, torch, pk, src):
     stage_ms = {k: sum(p[k] for p in per) / len(per) for k in per[0]}
     out = {"value": round(cfg.a_bytes / (ms / 1e3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
            "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
-           "roofline": roofline(cfg, step, stage_ms, pk["hbm_gbs"], src, "col"),
-           "note": "same A stored column-major; pass 1 (13 contiguous bits, D fused) + pass 2 fused with the "
-                   "gather: 3|A| of HBM traffic vs 7|A|; SA to 1e-12 (DESIGN.md R17)"}
+           "roofline": roofline(cfg, step, stage_ms, ms, pk["hbm_gbs"], src, layout),
+           "note": ("same A stored column-major; pass 1 (13 contiguous bits, D fused) + pass 2 fused with the "
+                    "gather: 3|A| of HBM traffic; SA to 1e-12 (DESIGN.md R17)" if layout == "col" else
+                    "same A stored row-major; tile FWHT passes + gather: (2 passes + 1)|A| of HBM traffic; "
+                    "SA bit-identical to the oracle")}
     del step, inputs
     return out
 
@@ -404,8 +463,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="C5")
-    ap.add_argument("--layout", default="row", choices=["row", "col"],
-                    help="storage of dense A: row-major (default) or column-major (the paper's LAPACK layout)")
+    ap.add_argument("--layout", default="auto", choices=["auto", "row", "col"],
+                    help="storage of dense A: row-major, column-major (the paper's LAPACK layout), or auto "
+                         "(default_layout: column-major for H D workloads whose row-major plan needs >= 3 passes)")
     ap.add_argument("--impl", default="skh", choices=["skh", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--sketch", default="hashing", choices=["hashing", "variant", "dht", "srdht"],
@@ -420,6 +480,8 @@ def main():
     cfg = configs.ALL[args.workload]
     if args.impl == "reference":
         return reference_arm(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
         if args.layout == "col":
@@ -428,7 +490,23 @@ def main():
         return sharded_bench.run(args, cfg)
     from paper_2105_11815_b200 import build
     build.build()
+    if args.layout == "auto":
+        args.layout = default_layout(cfg)
     return gpu_arm_single(args, cfg)
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` without a launcher: start N ranks with
+    torch.distributed.run on this node (127.0.0.1) and pass their output
+    through; rank 0 prints the JSON line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

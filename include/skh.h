@@ -103,9 +103,16 @@ double skh_c_ns(int64_t n_pad, int32_t s);
  *   bucket_signs[nrows*s] int8   its sign
  * The bucket lists are unique (a column hits a bucket at most once), so they are
  * compared bit-exactly with the oracle.  nrows == 0 gives bucket_ptr = 0.
- * The attempt cap (2^16 - 1 attempts per column) cannot be reached for s <= m
- * in practice; if it were, the column keeps fewer than s entries and
- * skh_hash_status() reports SKH_ERETRY.
+ * ATTEMPT CAP (read this if you never call skh_hash_status): attempts are capped
+ * at 2^16 - 1 per column.  The hardest column is s = m = 64 (s <= 64 is
+ * enforced): a coupon collector that misses one of 64 rows in 65535 attempts
+ * has probability <= 64 (63/64)^65535 < 1e-440, so the cap is unreachable for
+ * every legal (m, s).  If it were ever reached, the kernel would NOT stop
+ * short: it completes the column with the smallest unused rows (a
+ * deterministic fill that is NOT the canonical draw of R3, so S would differ
+ * from the oracle's) and raises a device flag; skh_hash_gen itself returns
+ * SKH_OK because the library never synchronises, and only skh_hash_status()
+ * (which synchronises) reports SKH_ERETRY.
  * ------------------------------------------------------------------------ */
 size_t skh_hash_workspace_bytes(int64_t nrows, int64_t m, int32_t s);
 int skh_hash_gen(uint64_t seed, int64_t m, int32_t s,

@@ -88,31 +88,29 @@ int64_t next_pow2(int64_t n) {
   return p;
 }
 
-// Library-owned copy stream per device (host-buffer variants overlap H2D with compute).
-cudaStream_t copy_stream() {
-  static std::mutex mu;
-  static cudaStream_t streams[64] = {};
+// Library-owned streams, one per calling THREAD and device, so calls from
+// several threads on different streams never couple through a shared library
+// stream (and a graph capture on one thread cannot pull in another thread's
+// work).  Created on first use, never destroyed (a few per thread).
+cudaStream_t thread_stream(int which) {
+  thread_local cudaStream_t streams[64][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
   if (dev < 0 || dev >= 64) return nullptr;
-  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-  return streams[dev];
+  if (!streams[dev][which] && cudaStreamCreateWithFlags(&streams[dev][which], cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    streams[dev][which] = nullptr;
+  }
+  return streams[dev][which];
 }
 
-// Side stream per device for independent small work (Sb = S b beside S A):
-// fork = the side stream waits for everything already on `st`; join = `st`
-// waits for the side stream.  Events are per thread and device.
-cudaStream_t side_stream() {
-  static std::mutex mu;
-  static cudaStream_t streams[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-  return streams[dev];
-}
+// Copy stream (host-buffer variants overlap H2D with compute).
+cudaStream_t copy_stream() { return thread_stream(0); }
+
+// Side stream for independent small work (Sb = S b beside S A): fork = the
+// side stream waits for everything already on `st`; join = `st` waits for the
+// side stream.  Streams and events are per thread and device.
+cudaStream_t side_stream() { return thread_stream(1); }
 
 cudaEvent_t side_event(int which) {
   thread_local cudaEvent_t ev[64][2] = {};
@@ -354,10 +352,11 @@ int skh_sketch_dense(int64_t m, int32_t s, const int32_t* bucket_ptr, const int3
   cudaStream_t st = as_stream(stream);
   // Sb (latency-bound, one warp per bucket) on the side stream beside S A
   cudaStream_t side = b ? side_fork(st) : st;
-  if (b && (rc = launch_gather_vec(m, bucket_ptr, bucket_rows, bucket_signs, b, Sb, alpha, side))) return rc;
-  rc = launch_gather_dense(m, bucket_ptr, bucket_rows, bucket_signs, d, A, lda, SA, ldsa, alpha, st);
-  if (rc) return rc;
-  return b ? side_join(st, side) : SKH_OK;
+  if (b) rc = launch_gather_vec(m, bucket_ptr, bucket_rows, bucket_signs, b, Sb, alpha, side);
+  if (!rc) rc = launch_gather_dense(m, bucket_ptr, bucket_rows, bucket_signs, d, A, lda, SA, ldsa, alpha, st);
+  // join on every path after the fork: the caller's stream stays ordered after the side work
+  const int jc = b ? side_join(st, side) : SKH_OK;
+  return rc ? rc : jc;
 }
 
 size_t skh_sketch_csr_workspace_bytes(int64_t nrows, int32_t s, int64_t nnz) {
@@ -390,11 +389,12 @@ int skh_sketch_csr(int64_t m, int32_t s, const int32_t* bucket_ptr, const int32_
   }
   cudaStream_t st = as_stream(stream);
   cudaStream_t side = b ? side_fork(st) : st;  // Sb beside the expand + reduce of S A
-  if (b && (rc = launch_gather_vec(m, bucket_ptr, bucket_rows, bucket_signs, b, Sb, alpha, side))) return rc;
-  rc = launch_gather_csr(m, s, bucket_ptr, bucket_rows, bucket_signs, nrows, d, nnz, row_ptr, col_idx, val, SA, ldsa,
-                         alpha, ws, st);
-  if (rc) return rc;
-  return b ? side_join(st, side) : SKH_OK;
+  if (b) rc = launch_gather_vec(m, bucket_ptr, bucket_rows, bucket_signs, b, Sb, alpha, side);
+  if (!rc)
+    rc = launch_gather_csr(m, s, bucket_ptr, bucket_rows, bucket_signs, nrows, d, nnz, row_ptr, col_idx, val, SA,
+                           ldsa, alpha, ws, st);
+  const int jc = b ? side_join(st, side) : SKH_OK;  // join on every path after the fork
+  return rc ? rc : jc;
 }
 
 size_t skh_rht_stages_workspace_bytes(int64_t nrows, int64_t nvalid, int64_t row0, int64_t d) {

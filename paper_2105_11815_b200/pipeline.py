@@ -21,13 +21,29 @@ def _ev():
 
 
 class _Timed:
-    """Records an event after each named stage (stage timing inside the timed region)."""
+    """Records an event after each named stage (stage timing inside the timed
+    region).  ``side`` names stages that run on a second stream, overlapped with
+    the main-stream stages: they are timed by events on that stream and reported
+    with an ``(overlapped)`` suffix, outside the main-stream sum."""
 
-    def __init__(self, names, record):
+    def __init__(self, names, record, side=()):
         self.names = list(names)
+        self.side = list(side)
         self.record = record
         self.events = [_ev() for _ in range(len(self.names) + 1)] if record else None
+        self.side_events = [_ev() for _ in range(len(self.side) + 1)] if (record and self.side) else None
         self.i = 0
+        self.j = 0
+
+    def side_start(self, stream):
+        if self.side_events:
+            self.side_events[0].record(stream)
+        self.j = 0
+
+    def side_mark(self, stream):
+        self.j += 1
+        if self.side_events:
+            self.side_events[self.j].record(stream)
 
     def start(self):
         if self.record:
@@ -41,7 +57,11 @@ class _Timed:
 
     def durations_ms(self):
         """Per-stage durations (call after synchronize)."""
-        return {n: self.events[k].elapsed_time(self.events[k + 1]) for k, n in enumerate(self.names)}
+        out = {n: self.events[k].elapsed_time(self.events[k + 1]) for k, n in enumerate(self.names)}
+        if self.side_events:
+            for k, n in enumerate(self.side):
+                out[n + " (overlapped)"] = self.side_events[k].elapsed_time(self.side_events[k + 1])
+        return out
 
 
 class HrhtStep:
@@ -74,14 +94,17 @@ class HrhtStep:
         import os
         self.side = torch.cuda.Stream(device=dev) if os.environ.get("SKH_PIPE_SIDE", "1") != "0" else None
         self.ws_b = api.rht_stages_workspace(n_pad, n, 0, 1, dev) if (self.side is not None and b is not None) else None
-        names = ["hash_gen"] + [f"fwht_pass{p}" for p in range(len(self.plan))]
+        # side-stream mode: the main stream's first stage is only the fork; the
+        # hash (and H D b) are timed on the side stream and reported as overlapped
+        names = ["fork" if self.side is not None else "hash_gen"] + [f"fwht_pass{p}" for p in range(len(self.plan))]
         if b is not None and self.side is None:
             names.append("fwht_b")
         names.append("gather")
-        self.timer = _Timed(names, record)
+        side = (["hash_gen"] + (["fwht_b"] if b is not None else [])) if self.side is not None else []
+        self.timer = _Timed(names, record, side)
 
     def new_timer(self):
-        return _Timed(self.timer.names, True)
+        return _Timed(self.timer.names, True, self.timer.side)
 
     def run(self, timer=None):
         t = timer or self.timer
@@ -110,10 +133,13 @@ class HrhtStep:
         main = torch.cuda.current_stream()
         self.side.wait_stream(main)
         with torch.cuda.stream(self.side):
+            t.side_start(self.side)
             self.bl = api.hash_gen(self.seed, self.m, self.s, self.n_pad, out=self.bl, variant=self.variant)
+            t.side_mark(self.side)
             if self.b is not None:
                 api.rht_stages(self.seed, self.b.view(-1, 1), 0, self.L, nrows=self.n_pad, apply_diag=True,
                                alpha=1.0, Y=self.yb, ws=self.ws_b)
+                t.side_mark(self.side)
         t.mark()
         lo = 0
         for p, k in enumerate(self.plan):

@@ -40,6 +40,14 @@ class CudaOps:
     def sketch_dense(self, bl, X, b, alpha, SA=None, Sb=None):
         return self.api.sketch_dense(bl, X, b, alpha=alpha, SA=SA, Sb=Sb)
 
+    def strip(self, bl, lo, hi):
+        """Buckets [lo, hi) of ``bl`` as bucket lists of their own: an offset
+        view of bucket_ptr (include/skh.h: ptr[0] need not be 0)."""
+        return self.api.BucketLists(hi - lo, bl.s, bl.nrows, bl.ptr[lo:hi + 1], bl.rows, bl.signs)
+
+    def sketch_csr(self, bl, row_ptr, col_idx, val, d, b, SA=None, Sb=None, ws=None):
+        return self.api.sketch_csr(bl, row_ptr, col_idx, val, d, b, SA=SA, Sb=Sb, ws=ws)
+
     def ordered_sum(self, parts, alpha, out=None):
         return self.api.ordered_sum(parts, alpha=alpha, out=out)
 
@@ -246,6 +254,10 @@ class ShardedHrhtM3:
             raise ValueError("A_loc must hold n / G rows")
         _log2(self.n)
         self.lg = _log2(self.L)
+        if self.n * self.s >= 2 ** 31:
+            # every rank draws and sorts the lists of all n columns (int32 entries)
+            raise ValueError(f"exchange-free H D needs n * s < 2^31 (n = {self.n}, s = {self.s}): "
+                             "use ShardedHrht (its ranks hash only their n / G rows)")
         self.A, self.b = A_loc, b_loc
         d = A_loc.shape[1]
         self.d = d
@@ -356,11 +368,12 @@ class ShardedPlain:
 class ShardedCsr:
     """CSR A replicated on every rank (|SA| >> |A| for C4): rank r computes the
     SA rows of its bucket strip, no collective; the strips
-    together are SA."""
+    together are SA.  The strip is handed to skh_sketch_csr as an offset view of
+    the full bucket_ptr, so every rank hashes all n rows once and reads only its
+    buckets' rows of A."""
 
-    def __init__(self, seed, row_ptr, col_idx, val, d, b, m, s, group=None):
-        from . import api
-        self.api = api
+    def __init__(self, seed, row_ptr, col_idx, val, d, b, m, s, ops=None, group=None):
+        self.ops = ops or CudaOps()
         self.G = dist.get_world_size(group)
         self.r = dist.get_rank(group)
         self.seed, self.m, self.s, self.d = seed, int(m), int(s), int(d)
@@ -372,20 +385,23 @@ class ShardedCsr:
         self.SA = torch.empty(max(hi - lo, 1), self.d, dtype=torch.float64, device=dev)
         self.Sb = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=dev) if b is not None else None
         self.bl = None
+        self.ws = None
+        if row_ptr.is_cuda:
+            from . import api
+            self.ws = api.sketch_csr_workspace(row_ptr.numel() - 1, self.s, val.numel(), dev)
 
     STAGES = ("hash_gen", "gather_csr")
 
     def run(self, mark=None):
         mark = mark or (lambda name: None)
-        api = self.api
+        ops = self.ops
         n = self.csr[0].numel() - 1
-        self.bl = api.hash_gen(self.seed, self.m, self.s, n, out=self.bl)
+        self.bl = ops.hash_gen(self.seed, self.m, self.s, n, 0, 0, 0, out=self.bl)
         mark("hash_gen")
         lo, hi = self.strips[self.r]
         if hi > lo:
-            strip = api.BucketLists(hi - lo, self.s, n, self.bl.ptr[lo:hi + 1], self.bl.rows, self.bl.signs)
-            api.sketch_csr(strip, *self.csr, self.d, self.b, SA=self.SA[: hi - lo],
-                           Sb=None if self.b is None else self.Sb[: hi - lo])
+            ops.sketch_csr(ops.strip(self.bl, lo, hi), *self.csr, self.d, self.b, SA=self.SA[: hi - lo],
+                           Sb=None if self.b is None else self.Sb[: hi - lo], ws=self.ws)
         mark("gather_csr")
         return self.SA[: hi - lo], None if self.b is None else self.Sb[: hi - lo], (lo, hi)
 

@@ -163,14 +163,18 @@ def run(args, cfg):
             # read every local row G s times (the folded H_G)
             L = cfg.n // G
             npass = len(api.rht_pass_plan((L).bit_length() - 1, cfg.d))
-            t = stage_ms["transform"]
-            alg = npass * 2 * L * cfg.d * 8
+            t = stage_ms["transform"] + stage_ms["gather"]
+            # per rank: the local passes read Z_r once each (d 8 B per
+            # row per launch), the gather reads every local row G s times (the
+            # folded H_G) and writes the partial m x d
+            alg = npass * L * cfg.d * 8 + G * cfg.s * L * cfg.d * 8 + cfg.m * cfg.d * 8
             ach = alg / (t / 1e3) / 1e9
-            line["roofline"] = {"bound": "hbm", "kernel": f"local FWHT passes per rank ({npass})",
+            line["roofline"] = {"bound": "hbm", "kernel": f"local FWHT passes ({npass}) + folded gather per rank",
                                 "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                                 "frac": round(ach / pk["hbm_gbs"], 4), "traffic": None, "peak_source": src,
                                 "gather_ms": round(stage_ms["gather"], 4),
-                                "gather_row_reads_per_local_row": G * cfg.s}
+                                "gather_row_reads_per_local_row": G * cfg.s,
+                                "gather_read_bytes_per_rank": G * cfg.s * L * cfg.d * 8}
             line["comm"] = {"all_to_all_rows_bytes_sent_per_rank": 0,
                             "strip_reduction_bytes_per_rank": (G - 1) * ((cfg.m + G - 1) // G) * cfg.d * 8}
         elif cfg.hd:

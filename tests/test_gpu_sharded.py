@@ -62,6 +62,18 @@ def _worker(rank, G, port, kind, out_dir):
         ok &= np.linalg.norm(SA - want) / np.linalg.norm(want) <= 1e-12
         if kind == "int":
             ok &= np.array_equal(SA, want)
+        # CSR A replicated, bucket strips through the offset view of bucket_ptr (M4)
+        from synth import configs
+        cfg = configs.C4.scaled(n=5000, d=300, m=97)
+        rp, ci, v = gen.csr(cfg)
+        bc = np.random.default_rng(3).standard_normal(cfg.n)
+        cs = sharded.ShardedCsr(cfg.seed, torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(),
+                                torch.from_numpy(v).cuda(), cfg.d, torch.from_numpy(bc).cuda(), cfg.m, cfg.s)
+        strip, sb, lohi = cs.run()
+        SA = sharded.gather_strips(strip, lohi, cfg.m).cpu().numpy()
+        Sb = sharded.gather_strips(sb, lohi, cfg.m).cpu().numpy()
+        want, wantb = sketch.sketch_csr(cfg.seed, rp, ci, v, cfg.d, bc, cfg.m, cfg.s)
+        ok &= np.array_equal(SA, want) and np.array_equal(Sb, wantb)
         with open(os.path.join(out_dir, f"r{rank}"), "w") as f:
             f.write("ok" if ok else "bad")
     finally:

@@ -17,7 +17,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import hadamard, hashing, sketch
-from synth import gen
+from synth import configs, gen
 
 
 class OracleOps:
@@ -47,6 +47,24 @@ class OracleOps:
         SA.copy_(torch.from_numpy(sketch.bucket_sum(X.numpy(), bl.ptr, bl.rows, bl.signs, alpha)))
         if b is not None:
             Sb.copy_(torch.from_numpy(sketch.bucket_sum(b.numpy(), bl.ptr, bl.rows, bl.signs, alpha)))
+        return SA, Sb
+
+    def strip(self, bl, lo, hi):
+        # the offset view the CUDA ops hand to skh_sketch_csr: ptr[lo..hi], absolute offsets into rows
+        return self.BL(hi - lo, bl.s, np.asarray(bl.ptr)[lo:hi + 1], bl.rows, bl.signs)
+
+    def sketch_csr(self, bl, row_ptr, col_idx, val, d, b, SA=None, Sb=None, ws=None):
+        rp, ci, v = row_ptr.numpy(), col_idx.numpy(), val.numpy()
+        c = hashing.c_s(bl.s)
+        for j in range(len(bl.ptr) - 1):
+            acc = np.zeros(d)
+            for t in range(int(bl.ptr[j]), int(bl.ptr[j + 1])):
+                acc += float(bl.signs[t]) * sketch.csr_row(rp, ci, v, int(bl.rows[t]), d)
+            SA[j] = torch.from_numpy(c * acc)
+        if b is not None:
+            Sb.copy_(torch.from_numpy(sketch.bucket_sum(b.numpy(), np.asarray(bl.ptr) - int(bl.ptr[0]),
+                                                        np.asarray(bl.rows)[int(bl.ptr[0]):],
+                                                        np.asarray(bl.signs)[int(bl.ptr[0]):], c)))
         return SA, Sb
 
     def ordered_sum(self, parts, alpha, out=None):
@@ -123,6 +141,16 @@ def _worker(rank, G, port, case):
             assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
             if kind == "int":
                 assert np.array_equal(got, ref)
+        # CSR A replicated, bucket strips (M4): every rank's strip through the
+        # offset view of bucket_ptr; together they are the oracle's SA, bit for bit
+        rp, ci, v = gen.csr(configs.C4.scaled(n=n, d=3 * d + 1, m=m))
+        cs = sharded.ShardedCsr(seed, torch.from_numpy(rp), torch.from_numpy(ci), torch.from_numpy(v), 3 * d + 1,
+                                torch.from_numpy(b.copy()), m, s, ops=ops)
+        strip, sb, (lo, hi) = cs.run()
+        SA = sharded.gather_strips(strip, (lo, hi), m).numpy()
+        Sb = sharded.gather_strips(sb, (lo, hi), m).numpy()
+        want, wantb = sketch.sketch_csr(seed, rp, ci, v, 3 * d + 1, b, m, s)
+        assert np.array_equal(SA, want) and np.array_equal(Sb, wantb)
     finally:
         dist.destroy_process_group()
 
