@@ -156,6 +156,88 @@ __global__ void __launch_bounds__(256, 3)
   }
 }
 
+// Persistent pass 1 for full chunks (nvalid covers every chunk, 16-byte
+// aligned columns): one CTA per SM walks chunks blockIdx.x, + gridDim.x, ...;
+// the next chunk is copied by cp.async straight into the other half of a
+// two-chunk shared-memory buffer (already in the swizzled exchange layout)
+// while this chunk's butterflies run in place in its half, so HBM reads stay
+// in flight across the compute.  Same stages, same order as cm_pass1_kernel.
+template <bool DIAG>
+__global__ void __launch_bounds__(256, 1)
+    cm_pass1p_kernel(const double* __restrict__ X, int64_t ldx, int64_t ncolX, const double* __restrict__ xb,
+                     double* __restrict__ Y, int64_t ldy, int64_t nchunks, int64_t total, uint64_t dkey,
+                     int64_t row0) {
+  extern __shared__ __align__(16) double2 smp[];  // [2][4096], swizzled
+  const int t = threadIdx.x;
+  auto issue = [&](int64_t item, int half) {
+    const int64_t c = item / nchunks;
+    const double2* src = reinterpret_cast<const double2*>(col_in(X, ldx, ncolX, xb, c) + ((item % nchunks) << kP1Bits));
+    double2* dsm = smp + half * 4096;
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {
+      const int q = t + 256 * v;
+      const unsigned d = (unsigned)__cvta_generic_to_shared(dsm + swz(q));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + q));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  int64_t item = blockIdx.x;
+  if (item < total) issue(item, 0);
+  for (int i = 0; item < total; item += gridDim.x, ++i) {
+    const int half = i & 1;
+    __syncthreads();  // every read of the other half (the previous chunk) is done
+    const int64_t next = item + gridDim.x;
+    if (next < total) {
+      issue(next, half ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();  // this chunk has landed
+    double2* sm = smp + half * 4096;
+    const int64_t c = item / nchunks;
+    const int64_t base = (item % nchunks) << kP1Bits;
+    double2 x[16];
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = sm[swz(v | (t << 4))];
+    if (DIAG) {
+      const int64_t g0 = row0 + base + 32 * t;
+      const int sh = (int)(g0 & 63);
+      uint64_t win = stream_u(dkey, (uint64_t)(g0 >> 6)) >> sh;
+      if (sh > 32) win |= stream_u(dkey, (uint64_t)((g0 >> 6) + 1)) << (64 - sh);
+      const uint32_t neg = (uint32_t)win;
+#pragma unroll
+      for (int v = 0; v < 16; ++v) {
+        if ((neg >> (2 * v)) & 1u) x[v].x = -x[v].x;
+        if ((neg >> (2 * v + 1)) & 1u) x[v].y = -x[v].y;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {  // element bit 0
+      const double a = x[v].x, b = x[v].y;
+      x[v] = make_double2(a + b, a - b);
+    }
+    stages16(x);  // element bits 1-4
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < 16; ++v) sm[swz(v | (t << 4))] = x[v];
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = sm[swz((t & 15) | (v << 4) | ((t >> 4) << 8))];
+    stages16(x);  // element bits 5-8
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < 16; ++v) sm[swz((t & 15) | (v << 4) | ((t >> 4) << 8))] = x[v];
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = sm[swz(t | (v << 8))];
+    stages16(x);  // element bits 9-12
+    double2* dst = reinterpret_cast<double2*>(Y + c * ldy + base);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) dst[t | (v << 8)] = x[v];
+  }
+}
+
 // Columns of at most 2^12 rows: the whole column in shared memory, stages one
 // at a time (small problems only).
 template <bool DIAG>
@@ -765,6 +847,19 @@ int launch_cm_pass1(uint64_t seed, const double* X, int64_t ldx, int64_t ncolX, 
   const bool vec = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(xb) |
                      reinterpret_cast<uintptr_t>(Y)) % 16 == 0) &&
                    (ldx % 2 == 0 || ncolX <= 1) && (ldy % 2 == 0);
+  if (vec && nvalid >= ((int64_t)1 << L)) {  // every chunk full: the persistent double-buffered kernel
+    const size_t smem = 2 * 65536;
+    const int64_t total = grid;
+    const int64_t g = std::min<int64_t>(total, (int64_t)num_sms());
+    int rc = apply_diag ? set_smem(cm_pass1p_kernel<true>, smem) : set_smem(cm_pass1p_kernel<false>, smem);
+    if (rc) return rc;
+    if (apply_diag)
+      cm_pass1p_kernel<true><<<(unsigned)g, 256, smem, st>>>(X, ldx, ncolX, xb, Y, ldy, nchunks, total, dkey, row0);
+    else
+      cm_pass1p_kernel<false><<<(unsigned)g, 256, smem, st>>>(X, ldx, ncolX, xb, Y, ldy, nchunks, total, dkey, row0);
+    note_launch();
+    return check_launch("cm_pass1p");
+  }
   const size_t smem = 65536;
 #define SKH_P1(D, V)                                                                                       \
   do {                                                                                                     \
