@@ -381,9 +381,10 @@ int skh_srdht_dense(uint64_t seed, int64_t n, int64_t m, int64_t d,
  * SYNCHRONISES `stream` and returns when x is ready.
  * Deterministic: fixed-order reductions.  ws: skh_lls_workspace_bytes (it
  * creates the per-thread cuSOLVER/cuBLAS handles, so it needs the device).
- * Errors: argument errors as usual (nothing enqueued); a rank-deficient SA
- * (some r_qq == 0) is detected after Step 2 and returns SKH_EINVAL with the
- * workspace already written and x untouched.
+ * Errors: argument errors as usual (nothing enqueued); a numerically
+ * rank-deficient SA (some |r_qq| <= 1e-12 max|r_jj| in the unpivoted QR) is
+ * detected after Step 2 and returns SKH_EINVAL with the workspace already
+ * written and x untouched -- skh_lls_solve_rr solves such problems.
  * Environment (read once per process, workspace query and solve alike):
  * SKH_LLS_HOSTLOOP=1 drives Step 4 from the host (bit-identical to the graph);
  * SKH_LLS_RINV=1 forms M = R^{-1} once (dtrsm against I, 2 d^2 doubles more
@@ -405,6 +406,35 @@ int skh_lls_solve_colmajor(int64_t n, int64_t d, const double* A, int64_t lda, c
                            double tau_a, double tau_r, int64_t it_max,
                            double* x, double* x_s, int64_t* info, double* stats,
                            void* ws, size_t ws_bytes, void* stream);
+
+/* Algorithm 1 with the paper's DEFAULT Step 2 (L1076-1077, L1109-1112): a
+ * column-pivoted, rank-revealing factorisation SA = Q R~ V^T (V = P) and
+ *     p = max{q : |r~_qq| >= rcond}     (1-based q; rcond absolute, default 1e-12),
+ * R11 = R~[:p, :p], Q1, V1 its first p columns (L873-886).  Computed as the
+ * Householder QR SA = Q0 R0 (cuSOLVER dgeqrf) followed by a column-pivoted
+ * Householder QR of the d x d factor, R0 P = Q1 R~ (the library's cooperative
+ * kernel, pivot = largest remaining column norm, LAPACK dgeqp3's norm
+ * downdating): SA P = (Q0 Q1) R~, the pivots of a CPQR of SA itself (Q0 keeps
+ * column norms).  Then Step 3 x_s = V1 R11^{-1} Q1^T Sb, Step 4 LSQR on
+ * W = A V1 R11^{-1} (applied as A (N y) and N^T (A^T u) with the d x d matrix
+ * N = P [R11^{-1} 0; 0 0]), Step 5 x = V1 R11^{-1} y: x has zeros outside the
+ * p pivoted coordinates; for rank-deficient A it attains the minimum residual
+ * (the objective, not x, is unique).  info[3] (host): step, LSQR iterations,
+ * p.  Workspace: skh_lls_rr_workspace_bytes (4 d^2 doubles more than
+ * skh_lls_workspace_bytes).  SKH_EINVAL for rcond < 0 and for d beyond the
+ * on-chip reflector of the pivoting kernel (d <= 27000).  Synchronises `stream`
+ * (Step 2 reads the d diagonal entries back to choose p). */
+size_t skh_lls_rr_workspace_bytes(int64_t n, int64_t d, int64_t m);
+int skh_lls_solve_rr(int64_t n, int64_t d, const double* A, int64_t lda, const double* b,
+                     int64_t m, const double* SA, int64_t ldsa, const double* Sb, double rcond,
+                     double tau_a, double tau_r, int64_t it_max,
+                     double* x, double* x_s, int64_t* info, double* stats,
+                     void* ws, size_t ws_bytes, void* stream);
+int skh_lls_solve_rr_colmajor(int64_t n, int64_t d, const double* A, int64_t lda, const double* b,
+                              int64_t m, const double* SA, int64_t ldsa, const double* Sb, double rcond,
+                              double tau_a, double tau_r, int64_t it_max,
+                              double* x, double* x_s, int64_t* info, double* stats,
+                              void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ *
  * Stage trace (thread-local).  After skh_trace_set(events, n) with n

@@ -1,4 +1,7 @@
 """Algorithm 1 Steps 2-5 (the sketch-preconditioned LLS solve), oracle side.
+Two Step-2 modes: the full-rank QR mode (below) and the paper's default,
+column-pivoted (R-CPQR) with rank truncation (``cpqr_sketch``, ``solve(...,
+rcond=...)``).
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
@@ -33,6 +36,20 @@ def qr_sketch(SA):
     """Step 2 (reading R19): SA = Q R with Q (m x d) orthonormal, R (d x d) upper."""
     Q, R = np.linalg.qr(np.asarray(SA, np.float64), mode="reduced")
     return Q, R
+
+
+def cpqr_sketch(SA, rcond=1e-12):
+    """Step 2, the paper's default mode: a column-
+    pivoted QR  SA P = Q R~  (LAPACK dgeqp3 via scipy: Businger-Golub
+    Householder QR with column pivoting; the paper's R-CPQR randomises the pivot
+    choice, reading R22), i.e. SA = Q R~ V^T with V = P, then
+        p = max{q : |r~_qq| >= rcond}      (1-based q; rcond absolute, as printed)
+    and R11 = R~[:p, :p], Q1 = Q[:, :p], V1 = P[:, :p] (Alg. 1 Step 2, L873-886).
+    Returns (Q1, R11, piv, p) with V1 = I[:, piv[:p]]."""
+    Q, R, piv = scipy.linalg.qr(np.asarray(SA, np.float64), mode="economic", pivoting=True)
+    big = np.nonzero(np.abs(np.diag(R)) >= rcond)[0]
+    p = int(big[-1]) + 1 if big.size else 0
+    return Q[:, :p], R[:p, :p], piv, p
 
 
 def solve_R(R, y):
@@ -100,20 +117,36 @@ def lsqr(Wmul, WTmul, b, tau_r, it_max):
     return y, it, test2, phibar
 
 
-def solve(A, b, SA, Sb, tau_a=1e-8, tau_r=1e-6, it_max=10000):
+def solve(A, b, SA, Sb, tau_a=1e-8, tau_r=1e-6, it_max=10000, rcond=None):
     """Algorithm 1 Steps 2-5 for dense A (n x d) given Step 1's SA, Sb.
 
+    rcond None: the full-rank QR mode (R19).  rcond given: the R-CPQR mode
+    (``cpqr_sketch``): x_s = V1 R11^{-1} Q1^T Sb (L881), LSQR on
+    W = A V1 R11^{-1} (L886-894), x = V1 R11^{-1} y (L896).
+
     Returns (x, info) with info = {"step": 3 or 4, "iters", "test2", "x_s",
-    "res_s" = ||A x_s - b||, "R"}."""
+    "res_s" = ||A x_s - b||, "R", "rank"}."""
     A = np.asarray(A, np.float64)
     b = np.asarray(b, np.float64)
-    Q, R = qr_sketch(SA)
-    x_s = solve_R(R, Q.T @ np.asarray(Sb, np.float64))
+    d = A.shape[1]
+    if rcond is None:
+        Q, R = qr_sketch(SA)
+        piv, p = np.arange(d), d
+    else:
+        Q, R, piv, p = cpqr_sketch(SA, rcond)
+
+    def V1(z):  # V1 z: the first p pivots' coordinates
+        x = np.zeros(d)
+        x[piv[:p]] = z
+        return x
+
+    x_s = V1(solve_R(R, Q.T @ np.asarray(Sb, np.float64)))
     res_s = float(np.linalg.norm(A @ x_s - b))
-    info = {"x_s": x_s, "res_s": res_s, "R": R}
-    if res_s <= tau_a:
+    info = {"x_s": x_s, "res_s": res_s, "R": R, "rank": p}
+    if res_s <= tau_a or p == 0:
         info.update(step=3, iters=0, test2=0.0)
         return x_s, info
-    y, it, test2, _ = lsqr(lambda v: A @ solve_R(R, v), lambda u: solve_RT(R, A.T @ u), b, tau_r, it_max)
+    Ap = A[:, piv[:p]]
+    y, it, test2, _ = lsqr(lambda v: Ap @ solve_R(R, v), lambda u: solve_RT(R, Ap.T @ u), b, tau_r, it_max)
     info.update(step=4, iters=it, test2=test2)
-    return solve_R(R, y), info
+    return V1(solve_R(R, y)), info

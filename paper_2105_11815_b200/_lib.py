@@ -72,6 +72,12 @@ SIGNATURES = {
                                      c_p, ctypes.POINTER(c_i64), ctypes.POINTER(c_d), c_p, c_sz, c_p]),
     "skh_lls_solve_colmajor": (ctypes.c_int, [c_i64, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_d, c_d, c_i64,
                                               c_p, c_p, ctypes.POINTER(c_i64), ctypes.POINTER(c_d), c_p, c_sz, c_p]),
+    "skh_lls_rr_workspace_bytes": (c_sz, [c_i64, c_i64, c_i64]),
+    "skh_lls_solve_rr": (ctypes.c_int, [c_i64, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_d, c_d, c_d, c_i64,
+                                        c_p, c_p, ctypes.POINTER(c_i64), ctypes.POINTER(c_d), c_p, c_sz, c_p]),
+    "skh_lls_solve_rr_colmajor": (ctypes.c_int, [c_i64, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p, c_d, c_d, c_d,
+                                                 c_i64, c_p, c_p, ctypes.POINTER(c_i64), ctypes.POINTER(c_d), c_p, c_sz,
+                                                 c_p]),
     "skh_trace_set": (ctypes.c_int, [ctypes.POINTER(c_p), ctypes.c_int]),
     "skh_trace_count": (ctypes.c_int, []),
     "skh_trace_name": (ctypes.c_char_p, [ctypes.c_int]),

@@ -421,15 +421,20 @@ class Trace:
 class LlsSolver:
     """x ~ argmin ||A x - b|| from Step 1's SA, Sb (skh_lls_solve; row-major A).
 
-    Defaults are the paper's."""
+    Defaults are the paper's.  rcond=None: the full-rank QR mode
+    (DGEQRF, L1077); rcond=1e-12: the paper's default rank-revealing Step 2
+    (column-pivoted QR, p = max{q : |r_qq| >= rcond}, L1109-1112;
+    skh_lls_solve_rr)."""
 
-    def __init__(self, n, d, m, device=None):
+    def __init__(self, n, d, m, device=None, rcond=None):
         lib = _lib.load()
         self.n, self.d, self.m = int(n), int(d), int(m)
+        self.rcond = rcond
         device = device or torch.device("cuda", torch.cuda.current_device())
-        nb = lib.skh_lls_workspace_bytes(self.n, self.d, self.m)
+        q = lib.skh_lls_workspace_bytes if rcond is None else lib.skh_lls_rr_workspace_bytes
+        nb = q(self.n, self.d, self.m)
         if nb == 0:
-            raise ValueError("skh_lls_workspace_bytes failed: " + lib.skh_last_error().decode())
+            raise ValueError("lls workspace query failed: " + lib.skh_last_error().decode())
         self.ws = _workspace(nb, device)
 
     def __call__(self, A, b, SA, Sb, tau_a=1e-8, tau_r=1e-6, it_max=10000, x=None, x_s=None, colmajor=False):
@@ -439,8 +444,18 @@ class LlsSolver:
         _need_cuda(A, b, SA, Sb)
         if x is None:
             x = torch.empty(self.d, dtype=torch.float64, device=A.device)
-        info = (ctypes.c_int64 * 2)()
+        info = (ctypes.c_int64 * 3)()
         stats = (ctypes.c_double * 3)()
+        if self.rcond is not None:
+            f = lib.skh_lls_solve_rr_colmajor if colmajor else lib.skh_lls_solve_rr
+            lda = _ld_cm(A, self.n) if colmajor else _ld(A)
+            ldsa = _ld_cm(SA, self.m) if colmajor else _ld(SA)
+            rc = f(self.n, self.d, _ptr(A), lda, _ptr(b), self.m, _ptr(SA), ldsa, _ptr(Sb), float(self.rcond),
+                   float(tau_a), float(tau_r), int(it_max), _ptr(x), _ptr(x_s), info, stats, _ptr(self.ws),
+                   self.ws.numel(), _stream())
+            _lib.check(rc, "skh_lls_solve_rr")
+            return x, {"step": int(info[0]), "iters": int(info[1]), "rank": int(info[2]), "test2": stats[0],
+                       "rnorm": stats[1], "res_s": stats[2]}
         if colmajor:
             rc = lib.skh_lls_solve_colmajor(self.n, self.d, _ptr(A), _ld_cm(A, self.n), _ptr(b), self.m, _ptr(SA),
                                             _ld_cm(SA, self.m), _ptr(Sb), float(tau_a), float(tau_r), int(it_max),
@@ -455,9 +470,9 @@ class LlsSolver:
                    "res_s": stats[2]}
 
 
-def lls_solve(A, b, SA, Sb, **kw):
+def lls_solve(A, b, SA, Sb, rcond=None, **kw):
     n, d = A.shape
-    return LlsSolver(n, d, SA.shape[0], A.device)(A, b, SA, Sb, **kw)
+    return LlsSolver(n, d, SA.shape[0], A.device, rcond=rcond)(A, b, SA, Sb, **kw)
 
 
 # ---------------------------------------------------------------- HR-DHT (eq. (6.1))

@@ -4,6 +4,13 @@
 //  Step 2  SA = Q R (full-rank Householder QR, the Blendenpik/DGEQRF mode the
 //          paper allows, L1077; reading R19): cuSOLVER dgeqrf on a
 //          column-major copy of SA -- a small dense factorisation (m x d).
+//          Rank-revealing mode (skh_lls_solve_rr; the paper's default R-CPQR
+//          with p = max{q : |r~_qq| >= rcond}, L1076-1077, L1109-1112; reading
+//          R22): SA = Q0 R0 as above, then a column-pivoted Householder QR of
+//          the d x d factor, R0 P = Q1 R~ (cpqr_kernel, ours), so SA P = (Q0 Q1) R~
+//          -- the pivots of a CPQR of SA itself, since Q0 preserves column norms.
+//          W = A V1 R11^{-1} is applied through N = P [R11^{-1} 0; 0 0] as a
+//          d x d GEMV (the R^{-1}-as-matrix path below).
 //  Step 3  x_s = R^{-1} Q^T Sb (cuSOLVER dormqr + cuBLAS dtrsv, a back-solve,
 //          L1081); stop if ||A x_s - b|| <= tau_a.
 //  Step 4  LSQR (Paige & Saunders) on W = A R^{-1} from y = 0, stopped by the
@@ -30,6 +37,7 @@
 //  norm / vector kernels on n- and d-vectors.
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 #include <cusolverDn.h>
 #include <math.h>
 #include <stdint.h>
@@ -458,6 +466,17 @@ struct LlsWs {
   double* Ri;      // SKH_LLS_RINV=1: M = R^{-1} column-major [d x d] (= M^T row-major)
   double* Rr;      // M row-major
   double* tmp;     // [d]
+  // rank-revealing mode (R-CPQR): the d x d factor being pivoted, R11, X = R11^{-1}
+  double* Rp;      // [d x d] column-major
+  double* Rc;      // [d x d] R11 gathered (column-major, ld d)
+  int* perm;       // [d] position -> physical column
+  int* pos_of;     // [d] physical column -> position (-1 while unpivoted)
+  double* tau1;    // [d] reflector scalars of the pivoted QR
+  double* nrm;     // [d] partial column norms^2
+  double* nrm0;    // [d] norms^2 at the last recompute
+  double* red_val; // [grid] argmax partials
+  int* red_idx;    // [grid]
+  double* diag;    // [d] |r~_qq|
   int64_t nblk, nrb;
   size_t total;
 };
@@ -481,7 +500,7 @@ bool rinv_mode() {
   return v;
 }
 
-LlsWs lls_layout(void* base, int64_t n, int64_t d, int64_t m, int lwork_n) {
+LlsWs lls_layout(void* base, int64_t n, int64_t d, int64_t m, int lwork_n, bool rr = false) {
   LlsWs w{};
   char* p = static_cast<char*>(base);
   size_t off = 0;
@@ -509,10 +528,22 @@ LlsWs lls_layout(void* base, int64_t n, int64_t d, int64_t m, int lwork_n) {
   w.devinfo = (int*)take(sizeof(int) * 4);
   w.lwork = (double*)take(sizeof(double) * (size_t)std::max(lwork_n, 1));
   w.lwork_n = lwork_n;
-  if (rinv_mode()) {
+  if (rinv_mode() || rr) {
     w.Ri = (double*)take(sizeof(double) * (size_t)d * d);
     w.Rr = (double*)take(sizeof(double) * (size_t)d * d);
     w.tmp = (double*)take(sizeof(double) * (size_t)d);
+  }
+  if (rr) {
+    w.Rp = (double*)take(sizeof(double) * (size_t)d * d);
+    w.Rc = (double*)take(sizeof(double) * (size_t)d * d);
+    w.perm = (int*)take(sizeof(int) * (size_t)d);
+    w.pos_of = (int*)take(sizeof(int) * (size_t)d);
+    w.tau1 = (double*)take(sizeof(double) * (size_t)d);
+    w.nrm = (double*)take(sizeof(double) * (size_t)d);
+    w.nrm0 = (double*)take(sizeof(double) * (size_t)d);
+    w.red_val = (double*)take(sizeof(double) * 1024);
+    w.red_idx = (int*)take(sizeof(int) * 1024);
+    w.diag = (double*)take(sizeof(double) * (size_t)d);
   }
   w.total = off;
   return w;
@@ -640,6 +671,298 @@ __global__ void identity_kernel(int64_t d, double* __restrict__ X) {
 }
 
 // M = R^{-1}: cuBLAS dtrsm of R X = I, then the row-major copy Rr
+// ------------------------------------------------------------------ Step 2, rank-revealing mode
+namespace cg = cooperative_groups;
+
+// Column-pivoted Householder QR (Businger-Golub, LAPACK dgeqp3's rule: pivot
+// = the largest remaining partial column norm, ties to the lower column;
+// norms downdated with dlaqp2's cancellation safeguard) of the d x d matrix
+// Rp (column-major, ld d), in place: R~ in the upper triangle of the pivoted
+// positions (entry (i, q) of R~ is Rp[i + perm[q] d] for i <= q), reflector q
+// below the diagonal of physical column perm[q] (unit leading entry implied),
+// tau1[q].  One cooperative grid: CTA bid owns physical columns bid, bid + G,
+// ...; per pivot two grid syncs (argmax partials; the new reflector), and each
+// warp applies the reflector to one owned column at a time.
+__global__ void __launch_bounds__(256) cpqr_kernel(int d, double* __restrict__ Rp, int* __restrict__ perm,
+                                                   int* __restrict__ pos_of, double* __restrict__ tau1,
+                                                   double* __restrict__ nrm, double* __restrict__ nrm0,
+                                                   double* __restrict__ red_val, int* __restrict__ red_idx) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double vsh[];  // [d] the current reflector
+  __shared__ double wv[8];
+  __shared__ int wi[8];
+  __shared__ double hs[2];
+  const int G = gridDim.x, bid = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const double tol3z = 1.4901161193847656e-08;  // sqrt(DBL_EPSILON), dlaqp2
+  auto col = [&](int c) { return Rp + (int64_t)c * d; };
+  // initial norms of the owned columns (one warp per column)
+  for (int c = bid + G * wp; c < d; c += 8 * G) {
+    const double* a = col(c);
+    double s = 0.0;
+    for (int i = lane; i < d; i += 32) s += a[i] * a[i];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      nrm[c] = s;
+      nrm0[c] = s;
+      pos_of[c] = -1;
+    }
+  }
+  grid.sync();
+  for (int k = 0; k < d; ++k) {
+    // (a) argmax of the remaining partial norms over the owned columns
+    double best = -1.0;
+    int bc = 0x7fffffff;
+    for (int c = bid + G * tid; c < d; c += G * 256) {
+      if (pos_of[c] >= 0) continue;
+      const double v = nrm[c];
+      if (v > best || (v == best && c < bc)) {
+        best = v;
+        bc = c;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (ov > best || (ov == best && oc < bc)) {
+        best = ov;
+        bc = oc;
+      }
+    }
+    if (lane == 0) {
+      wv[wp] = best;
+      wi[wp] = bc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int q = 1; q < 8; ++q)
+        if (wv[q] > best || (wv[q] == best && wi[q] < bc)) {
+          best = wv[q];
+          bc = wi[q];
+        }
+      red_val[bid] = best;
+      red_idx[bid] = bc;
+    }
+    grid.sync();
+    // (b) the global pivot (every CTA computes the same), its reflector by the owner
+    best = -1.0;
+    bc = 0x7fffffff;
+    for (int q = tid; q < G; q += 256) {
+      const double v = red_val[q];
+      const int c = red_idx[q];
+      if (v > best || (v == best && c < bc)) {
+        best = v;
+        bc = c;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (ov > best || (ov == best && oc < bc)) {
+        best = ov;
+        bc = oc;
+      }
+    }
+    __syncthreads();  // wv/wi reuse
+    if (lane == 0) {
+      wv[wp] = best;
+      wi[wp] = bc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int q = 1; q < 8; ++q)
+        if (wv[q] > best || (wv[q] == best && wi[q] < bc)) {
+          best = wv[q];
+          bc = wi[q];
+        }
+      wi[0] = bc;
+    }
+    __syncthreads();
+    const int cs = wi[0];
+    if (cs % G == bid) {
+      double* a = col(cs);
+      double s = 0.0;  // ||x(k+1:)||^2
+      for (int i = k + 1 + tid; i < d; i += 256) s += a[i] * a[i];
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      __syncthreads();
+      if (lane == 0) wv[wp] = s;
+      __syncthreads();
+      if (tid == 0) {
+        double xn2 = 0.0;
+        for (int q = 0; q < 8; ++q) xn2 += wv[q];
+        const double alpha = a[k];
+        double tau = 0.0, beta = alpha, scal = 0.0;
+        if (xn2 > 0.0) {  // dlarfg: beta = -sign(alpha) ||x||, tau = (beta - alpha) / beta, v = x / (alpha - beta)
+          beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+          tau = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
+        hs[0] = scal;
+        hs[1] = beta;
+        tau1[k] = tau;
+        perm[k] = cs;
+        pos_of[cs] = k;
+      }
+      __syncthreads();
+      const double scal = hs[0];
+      for (int i = k + 1 + tid; i < d; i += 256) a[i] *= scal;
+      if (tid == 0) a[k] = hs[1];
+    }
+    grid.sync();
+    // (c) apply H_k = I - tau v v^T to the owned unpivoted columns, downdate their norms
+    const double* v = col(cs);
+    for (int i = k + 1 + tid; i < d; i += 256) vsh[i] = v[i];
+    if (tid == 0) vsh[k] = 1.0;
+    __syncthreads();
+    const double tau = tau1[k];
+    for (int c = bid + G * wp; c < d; c += 8 * G) {
+      if (pos_of[c] >= 0) continue;
+      double* a = col(c);
+      double s = 0.0;
+      for (int i = k + lane; i < d; i += 32) s += vsh[i] * a[i];
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      const double tw = tau * s;
+      if (tw != 0.0)
+        for (int i = k + lane; i < d; i += 32) a[i] -= tw * vsh[i];
+      __syncwarp();
+      // dlaqp2 norm downdate
+      double nv = nrm[c];
+      if (nv != 0.0) {
+        const double rk = a[k];
+        double temp = 1.0 - rk * rk / nv;
+        temp = temp < 0.0 ? 0.0 : temp;
+        if (temp * (nv / nrm0[c]) <= tol3z) {
+          double r2 = 0.0;
+          for (int i = k + 1 + lane; i < d; i += 32) r2 += a[i] * a[i];
+          for (int o = 16; o; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+          nv = r2;
+          if (lane == 0) nrm0[c] = r2;
+        } else {
+          nv *= temp;
+        }
+        if (lane == 0) nrm[c] = nv;
+      }
+      __syncwarp();
+    }
+    __syncthreads();  // vsh is rewritten next step
+  }
+}
+
+// |r~_qq| per position
+__global__ void cpqr_diag_kernel(int d, const double* __restrict__ Rp, const int* __restrict__ perm,
+                                 double* __restrict__ diag) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < d) diag[q] = fabs(Rp[q + (int64_t)perm[q] * d]);
+}
+
+// R11 (p x p, upper) gathered into Rc (column-major, ld d); Xb = I_p (ld d) in Ri
+__global__ void cpqr_r11_kernel(int d, int p, const double* __restrict__ Rp, const int* __restrict__ perm,
+                                double* __restrict__ Rc, double* __restrict__ X) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)p * p) return;
+  const int i = (int)(t % p), j = (int)(t / p);
+  Rc[i + (int64_t)j * d] = i <= j ? Rp[i + (int64_t)perm[j] * d] : 0.0;
+  X[i + (int64_t)j * d] = i == j ? 1.0 : 0.0;
+}
+
+// the upper triangle of F (m x d, ld m) into Rp (d x d, ld d), zeros below
+__global__ void upper_copy_kernel(int64_t d, const double* __restrict__ F, int64_t m, double* __restrict__ Rp) {
+  const int64_t j = (int64_t)blockIdx.x * 32 + threadIdx.x;  // column
+  for (int64_t i = (int64_t)blockIdx.y * 32 + threadIdx.y; i < (int64_t)blockIdx.y * 32 + 32; i += 8)
+    if (i < d && j < d) Rp[i + j * d] = i <= j ? F[i + j * m] : 0.0;
+}
+
+// N = P [X 0; 0 0] (column-major d x d, zeroed first): N[perm[i], j] = X[i, j] for i, j < p
+__global__ void cpqr_scatter_kernel(int d, int p, const double* __restrict__ X, const int* __restrict__ perm,
+                                     double* __restrict__ N) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)p * p) return;
+  const int i = (int)(t % p), j = (int)(t / p);
+  N[perm[i] + (int64_t)j * d] = X[i + (int64_t)j * d];
+}
+
+// z <- Q1^T z = H_{d-1} ... H_0 z (z: first d entries of Q0^T Sb), one CTA
+__global__ void __launch_bounds__(256) cpqr_qt_kernel(int d, const double* __restrict__ Rp,
+                                                      const int* __restrict__ perm, const double* __restrict__ tau1,
+                                                      double* __restrict__ z) {
+  __shared__ double ws[8];
+  __shared__ double tw;
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  for (int k = 0; k < d; ++k) {
+    const double* v = Rp + (int64_t)perm[k] * d;
+    double s = 0.0;
+    for (int i = k + tid; i < d; i += 256) s += (i == k ? 1.0 : v[i]) * z[i];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) ws[wp] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int q = 0; q < 8; ++q) t += ws[q];
+      tw = tau1[k] * t;
+    }
+    __syncthreads();
+    const double c = tw;
+    for (int i = k + tid; i < d; i += 256) z[i] -= c * (i == k ? 1.0 : v[i]);
+    __syncthreads();
+  }
+}
+
+// Rank-revealing Step 2 on the dgeqrf factor in w.F: returns p (host) and
+// leaves N (Ri, column-major) and N^T (Rr, row-major view) for trsv's GEMV path.
+int cpqr_step2(Handles* h, int64_t d, int64_t m, const LlsWs& w, double rcond, cudaStream_t st, int64_t* p_out) {
+  const int di = (int)d;
+  // R0: the upper triangle of F (ld m) -> Rp (ld d), zeros below
+  dim3 grid((unsigned)((d + 31) / 32), (unsigned)((d + 31) / 32));
+  upper_copy_kernel<<<grid, dim3(32, 8), 0, st>>>(d, w.F, m, w.Rp);
+  note_launch();
+  int nsm = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = sizeof(double) * (size_t)d;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("lls cpqr: d = %lld too large for the on-chip reflector", (long long)d);
+    return SKH_EINVAL;
+  }
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cpqr_kernel, 256, smem);
+  int G = std::min(nsm * std::max(per, 1), std::min(1024, std::max(1, di)));
+  G = std::min(G, nsm);  // one CTA per SM: enough columns per CTA, cheap grid syncs
+  void* args[] = {(void*)&di, (void*)&w.Rp, (void*)&w.perm, (void*)&w.pos_of, (void*)&w.tau1,
+                  (void*)&w.nrm, (void*)&w.nrm0, (void*)&w.red_val, (void*)&w.red_idx};
+  if (cudaLaunchCooperativeKernel((const void*)cpqr_kernel, dim3(G), dim3(256), args, smem, st) != cudaSuccess)
+    return check_launch("lls: cpqr");
+  note_launch();
+  cpqr_diag_kernel<<<(unsigned)((d + 255) / 256), 256, 0, st>>>(di, w.Rp, w.perm, w.diag);
+  note_launch();
+  std::vector<double> dg((size_t)d);
+  if (cudaMemcpyAsync(dg.data(), w.diag, sizeof(double) * (size_t)d, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return check_launch("lls: cpqr diagonal");
+  int64_t p = 0;  // p = max{q : |r~_qq| >= rcond} (1-based q), L1109-1112
+  for (int64_t q = 0; q < d; ++q)
+    if (dg[q] >= rcond) p = q + 1;
+  *p_out = p;
+  // N = P [R11^{-1} 0; 0 0]
+  const int pi = (int)p;
+  cudaMemsetAsync(w.Ri, 0, sizeof(double) * (size_t)d * d, st);
+  if (p > 0) {
+    cpqr_r11_kernel<<<(unsigned)((p * p + 255) / 256), 256, 0, st>>>(di, pi, w.Rp, w.perm, w.Rc, w.Rr);
+    note_launch();
+    const double one = 1.0;
+    if (cublasDtrsm(h->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, pi, pi, &one,
+                    w.Rc, di, w.Rr, di) != CUBLAS_STATUS_SUCCESS) {
+      set_error("lls: cublasDtrsm (R11^{-1}) failed");
+      return SKH_ECUDA;
+    }
+    cpqr_scatter_kernel<<<(unsigned)((p * p + 255) / 256), 256, 0, st>>>(di, pi, w.Rr, w.perm, w.Ri);
+    note_launch();
+  }
+  to_colmajor_kernel<<<grid, dim3(32, 8), 0, st>>>(d, d, w.Ri, d, w.Rr);  // Rr = row-major N
+  note_launch();
+  return check_launch("lls: cpqr N");
+}
+
 int form_rinv(Handles* h, int64_t d, const LlsWs& w, int64_t m, cudaStream_t st) {
   identity_kernel<<<(unsigned)((d * d + 255) / 256), 256, 0, st>>>(d, w.Ri);
   note_launch();
@@ -780,10 +1103,17 @@ size_t skh_lls_workspace_bytes(int64_t n, int64_t d, int64_t m) {
   return lls_layout(nullptr, n, d, m, lw).total;
 }
 
+size_t skh_lls_rr_workspace_bytes(int64_t n, int64_t d, int64_t m) {
+  if (n < 1 || d < 1 || m < d || m >= (1ll << 31) || d >= (1ll << 31)) return 0;
+  int lw = 0;
+  if (query_lwork(m, d, &lw)) return 0;
+  return lls_layout(nullptr, n, d, m, lw, true).total;
+}
+
 static int lls_solve_impl(bool cm, int64_t n, int64_t d, const double* A, int64_t lda, const double* b, int64_t m,
                           const double* SA, int64_t ldsa, const double* Sb, double tau_a, double tau_r,
                           int64_t it_max, double* x, double* x_s, int64_t* info, double* stats, void* ws,
-                          size_t ws_bytes, void* stream) {
+                          size_t ws_bytes, void* stream, bool rr = false, double rcond = 0.0) {
   if (n < 1 || d < 1 || m < d || !A || !b || !SA || !Sb || !x || !info || !stats || it_max < 0 || tau_r < 0 ||
       m >= (1ll << 31)) {
     set_error("lls_solve: need n, d >= 1, m >= d, A, b, SA, Sb, x, info, stats, it_max >= 0");
@@ -793,10 +1123,14 @@ static int lls_solve_impl(bool cm, int64_t n, int64_t d, const double* A, int64_
     set_error(cm ? "lls_solve_colmajor: lda < n or ldsa < m" : "lls_solve: lda/ldsa < d");
     return SKH_EDIM;
   }
+  if (rr && !(rcond >= 0.0)) {
+    set_error("lls_solve_rr: rcond must be >= 0");
+    return SKH_EINVAL;
+  }
   int lw = 0;
   int rc = query_lwork(m, d, &lw);
   if (rc) return rc;
-  const LlsWs w = lls_layout(ws, n, d, m, lw);
+  const LlsWs w = lls_layout(ws, n, d, m, lw, rr);
   if (!ws || ws_bytes < w.total) {
     set_error("lls_solve workspace too small: need %zu bytes", w.total);
     return SKH_EWORKSPACE;
@@ -823,22 +1157,31 @@ static int lls_solve_impl(bool cm, int64_t n, int64_t d, const double* A, int64_
       return SKH_ECUDA;
     }
   }
-  // rank check: the full-rank QR mode needs every r_qq != 0
-  {
+  int64_t p = d;
+  if (rr) {
+    // rank-revealing mode: pivoted QR of R0, p from rcond, N = P [R11^{-1} 0; 0 0]
+    if ((rc = cpqr_step2(h, d, m, w, rcond, st, &p))) return rc;
+    info[2] = p;
+  } else {
+    // full-rank QR mode (R19): reject a rank-deficient SA -- a diagonal entry
+    // |r_qq| < 1e-12 max|r_jj| (relative: the unpivoted QR is not rank
+    // revealing, the rank-revealing mode is skh_lls_solve_rr)
     std::vector<double> diag((size_t)d);
     if (cudaMemcpy2DAsync(diag.data(), sizeof(double), w.F, sizeof(double) * (size_t)(m + 1), sizeof(double), d,
                           cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
       return check_launch("lls: R diagonal");
+    double rmax = 0.0;
+    for (int64_t q = 0; q < d; ++q) rmax = std::max(rmax, fabs(diag[q]));
     for (int64_t q = 0; q < d; ++q) {
-      if (!(fabs(diag[q]) > 0.0)) {
-        set_error("lls: SA is rank deficient (r_%lld,%lld = %g); the full-rank QR mode needs rank d", (long long)q,
-                  (long long)q, diag[q]);
+      if (!(fabs(diag[q]) > 1e-12 * rmax)) {
+        set_error("lls: SA is numerically rank deficient (|r_%lld,%lld| = %g <= 1e-12 max|r_jj|); the full-rank QR "
+                  "mode needs rank d -- use skh_lls_solve_rr", (long long)q, (long long)q, diag[q]);
         return SKH_EINVAL;
       }
     }
+    if (w.Ri && (rc = form_rinv(h, d, w, m, st))) return rc;
   }
-  if (w.Ri && (rc = form_rinv(h, d, w, m, st))) return rc;
   skh_trace_mark(st, "qr");
   // ---- Step 3: x_s = R^{-1} Q^T Sb
   cudaMemcpyAsync(w.qtb, Sb, sizeof(double) * (size_t)m, cudaMemcpyDeviceToDevice, st);
@@ -847,8 +1190,12 @@ static int lls_solve_impl(bool cm, int64_t n, int64_t d, const double* A, int64_
     set_error("lls: cusolverDnDormqr failed");
     return SKH_ECUDA;
   }
+  if (rr) {  // Q^T Sb = Q1^T (Q0^T Sb): the pivoted QR's reflectors on the first d entries
+    cpqr_qt_kernel<<<1, 256, 0, st>>>((int)d, w.Rp, w.perm, w.tau1, w.qtb);
+    note_launch();
+  }
   cudaMemcpyAsync(w.xs, w.qtb, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);
-  if ((rc = trsv(h, d, w, m, false, w.xs))) return rc;
+  if ((rc = trsv(h, d, w, m, false, w.xs))) return rc;  // R^{-1} z, or N z = V1 R11^{-1} z_1..p
   if (x_s) cudaMemcpyAsync(x_s, w.xs, sizeof(double) * (size_t)d, cudaMemcpyDeviceToDevice, st);
   if ((rc = apply_A(cm, n, d, A, lda, w.xs, -1.0, b, w.u, w, 0, st))) return rc;  // u = A x_s - b
   double res2 = 0.0;
@@ -963,6 +1310,22 @@ int skh_lls_solve(int64_t n, int64_t d, const double* A, int64_t lda, const doub
                   double* x_s, int64_t* info, double* stats, void* ws, size_t ws_bytes, void* stream) {
   return lls_solve_impl(false, n, d, A, lda, b, m, SA, ldsa, Sb, tau_a, tau_r, it_max, x, x_s, info, stats, ws,
                         ws_bytes, stream);
+}
+
+int skh_lls_solve_rr(int64_t n, int64_t d, const double* A, int64_t lda, const double* b, int64_t m,
+                     const double* SA, int64_t ldsa, const double* Sb, double rcond, double tau_a, double tau_r,
+                     int64_t it_max, double* x, double* x_s, int64_t* info, double* stats, void* ws,
+                     size_t ws_bytes, void* stream) {
+  return lls_solve_impl(false, n, d, A, lda, b, m, SA, ldsa, Sb, tau_a, tau_r, it_max, x, x_s, info, stats, ws,
+                        ws_bytes, stream, true, rcond);
+}
+
+int skh_lls_solve_rr_colmajor(int64_t n, int64_t d, const double* A, int64_t lda, const double* b, int64_t m,
+                              const double* SA, int64_t ldsa, const double* Sb, double rcond, double tau_a,
+                              double tau_r, int64_t it_max, double* x, double* x_s, int64_t* info, double* stats,
+                              void* ws, size_t ws_bytes, void* stream) {
+  return lls_solve_impl(true, n, d, A, lda, b, m, SA, ldsa, Sb, tau_a, tau_r, it_max, x, x_s, info, stats, ws,
+                        ws_bytes, stream, true, rcond);
 }
 
 int skh_lls_solve_colmajor(int64_t n, int64_t d, const double* A, int64_t lda, const double* b, int64_t m,

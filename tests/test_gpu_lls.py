@@ -112,14 +112,86 @@ def test_lls_it_max_and_tau():
     assert info["test2"] <= 1e-14
 
 
-def test_lls_rank_deficient_is_rejected():
+def test_lls_rank_deficient_is_rejected_in_full_rank_mode():
+    """The full-rank (DGEQRF) mode refuses a numerically rank-deficient SA -- a
+    zero column, and a column that is a linear combination of others (its r_qq
+    is ~1e-16 ||SA||, not 0: the relative test catches it)."""
     from oracle import sketch
-    A, b = ill_conditioned(1000, 10, 5)
-    A[:, 3] = 0.0
-    SA, Sb = sketch.sketch_dense(1, A, b, 40, 2)
-    with pytest.raises(Exception, match="rank deficient"):
-        skh().lls_solve(torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), torch.from_numpy(SA).cuda(),
-                        torch.from_numpy(Sb).cuda())
+    for kind in ("zero", "combination"):
+        A, b = ill_conditioned(1000, 10, 5)
+        if kind == "zero":
+            A[:, 3] = 0.0
+        else:
+            A[:, 6] = 2.0 * A[:, 1] - A[:, 4]
+        SA, Sb = sketch.sketch_dense(1, A, b, 40, 2)
+        with pytest.raises(Exception, match="rank deficient"):
+            skh().lls_solve(torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(), torch.from_numpy(SA).cuda(),
+                            torch.from_numpy(Sb).cuda())
+
+
+def deficient(n, d, r, seed, scale=1.0):
+    """A of exact rank r: r independent columns, d - r combinations, shuffled."""
+    g = np.random.default_rng(seed)
+    B = scale * g.standard_normal((n, r))
+    C = g.standard_normal((r, d - r))
+    A = np.ascontiguousarray(np.concatenate([B, B @ C], axis=1)[:, g.permutation(d)])
+    return A, g.standard_normal(n)
+
+
+@pytest.mark.parametrize("n,d,r,m,s", [(2500, 30, 18, 100, 2), (5000, 64, 1, 120, 1), (4096, 200, 150, 350, 2),
+                                       (3000, 40, 40, 90, 3), (2000, 12, 0, 30, 1)])
+def test_lls_rank_revealing_vs_oracle(n, d, r, m, s):
+    """The paper's default Step 2 (R-CPQR, p = max{q : |r_qq| >= 1e-12},
+    L1076-1077, L1109-1112) through skh_lls_solve_rr vs oracle/lls.py's
+    scipy-dgeqp3 reading: the same rank p; x zero outside the p pivoted
+    coordinates; the least-squares objective within 1e-10 of the minimum-norm
+    lstsq residual (the objective is unique, x is not); x_s's residual vs the
+    oracle's.  r = d: full rank (then also the QR mode's objective); r = 0: A = 0."""
+    from oracle import lls, sketch
+    A, b = deficient(n, d, r, 7 + d) if r > 0 else (np.zeros((n, d)), np.random.default_rng(1).standard_normal(n))
+    SA, Sb = sketch.sketch_dense(3, A, b, m, s)
+    At, bt = torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda()
+    xs = torch.empty(d, dtype=torch.float64, device="cuda")
+    x, info = skh().LlsSolver(n, d, m, rcond=1e-12)(At, bt, torch.from_numpy(SA).cuda(), torch.from_numpy(Sb).cuda(),
+                                                    x_s=xs, tau_a=0.0, tau_r=1e-14, it_max=2000)
+    xo, io = lls.solve(A, b, SA, Sb, tau_a=0.0, tau_r=1e-14, it_max=2000, rcond=1e-12)
+    assert info["rank"] == io["rank"] == np.linalg.matrix_rank(A)
+    rmin = np.linalg.norm(A @ np.linalg.lstsq(A, b, rcond=None)[0] - b)
+    got = np.linalg.norm(A @ np_(x) - b)
+    assert abs(got - rmin) <= 1e-10 * max(rmin, 1.0)
+    assert abs(info["res_s"] - io["res_s"]) <= 1e-8 * max(io["res_s"], 1.0)
+    p = info["rank"]
+    nz = np.nonzero(np_(x))[0]
+    assert len(nz) <= p
+    if r == d:
+        x2, _ = skh().lls_solve(At, bt, torch.from_numpy(SA).cuda(), torch.from_numpy(Sb).cuda(), tau_a=0.0,
+                                tau_r=1e-14, it_max=2000)
+        assert abs(np.linalg.norm(A @ np_(x2) - b) - got) <= 1e-10 * max(rmin, 1.0)
+
+
+def test_lls_rank_revealing_rcond_truncation_and_colmajor():
+    """rcond between two pivoted diagonals drops exactly the pivots below it
+    (same p as the oracle), and the column-major entry point agrees."""
+    from oracle import lls, sketch
+    A, b = ill_conditioned(3000, 24, 8, cond=1e9)
+    SA, Sb = sketch.sketch_dense(2, A, b, 80, 2)
+    import scipy.linalg
+    R = scipy.linalg.qr(SA, mode="economic", pivoting=True)[1]
+    dg = np.abs(np.diag(R))
+    rc = float(np.sqrt(dg[-4] * dg[-3]))
+    kw = dict(tau_a=0.0, tau_r=1e-12, it_max=3000)
+    x, info = skh().LlsSolver(3000, 24, 80, rcond=rc)(torch.from_numpy(A).cuda(), torch.from_numpy(b).cuda(),
+                                                      torch.from_numpy(SA).cuda(), torch.from_numpy(Sb).cuda(), **kw)
+    xo, io = lls.solve(A, b, SA, Sb, rcond=rc, **kw)
+    assert info["rank"] == io["rank"] == 21
+    xc, ic = skh().LlsSolver(3000, 24, 80, rcond=rc)(torch.from_numpy(np.ascontiguousarray(A.T)).cuda(),
+                                                     torch.from_numpy(b).cuda(),
+                                                     torch.from_numpy(np.ascontiguousarray(SA.T)).cuda(),
+                                                     torch.from_numpy(Sb).cuda(), colmajor=True, **kw)
+    assert ic["rank"] == 21
+    ro = np.linalg.norm(A @ xo - b)
+    for xx in (x, xc):
+        assert abs(np.linalg.norm(A @ np_(xx) - b) - ro) <= 1e-9 * ro
 
 
 def test_lls_deterministic_and_C2_full_size():

@@ -111,3 +111,63 @@ def test_hashing_preconditioner_at_paper_m():
     x, info = lls.solve(A, b, SA, Sb)
     assert info["step"] == 4 and info["iters"] < 60
     assert hashing.c_s(1) == 1.0
+
+
+# ------------------------------------------------------------------ R-CPQR mode
+def deficient(n=2500, d=30, r=18, m=100, s=2, seed=11):
+    """A of exact rank r < d: r independent columns and d - r combinations of them."""
+    g = np.random.default_rng(seed)
+    B = g.standard_normal((n, r))
+    C = g.standard_normal((r, d - r))
+    A = np.concatenate([B, B @ C], axis=1)[:, g.permutation(d)]
+    b = g.standard_normal(n)
+    SA, Sb = sketch.sketch_dense(seed, A, b, m, s)
+    return A, b, SA, Sb, r
+
+
+def test_cpqr_rank_and_factorisation():
+    """SA P = Q R~ exactly (to rounding); the detected p equals rank(A) for an
+    exactly rank-deficient A (S is an embedding at m = 100 >> r); r~_qq beyond
+    p are at the rounding level and non-increasing |r~_qq| (Businger-Golub)."""
+    A, b, SA, Sb, r = deficient()
+    Q1, R11, piv, p = lls.cpqr_sketch(SA, 1e-12)
+    assert p == r == np.linalg.matrix_rank(A)
+    Q, R, piv2 = __import__("scipy.linalg").linalg.qr(SA, mode="economic", pivoting=True)
+    assert np.allclose(SA[:, piv2], Q @ R, atol=1e-12 * np.linalg.norm(SA))
+    dg = np.abs(np.diag(R))
+    assert np.all(dg[1:] <= dg[:-1] * (1 + 1e-12))
+    assert dg[p - 1] >= 1e-12 > dg[p] if p < len(dg) else True
+
+
+def test_cpqr_solve_reaches_the_least_squares_residual():
+    """Rank-deficient A: x is not unique, but the objective is.  The R-CPQR solve
+    reaches the minimum residual of numpy's minimum-norm lstsq (the
+    solution is optimal over the detected column space), and x_tau lies in the
+    span of the p pivoted coordinates."""
+    A, b, SA, Sb, r = deficient(seed=12)
+    x, info = lls.solve(A, b, SA, Sb, tau_a=0.0, tau_r=1e-14, it_max=500, rcond=1e-12)
+    xm = np.linalg.lstsq(A, b, rcond=None)[0]
+    rmin = np.linalg.norm(A @ xm - b)
+    assert info["rank"] == r and info["step"] == 4
+    assert abs(np.linalg.norm(A @ x - b) - rmin) <= 1e-10 * rmin
+    Q1, R11, piv, p = lls.cpqr_sketch(SA, 1e-12)
+    assert np.all(x[piv[p:]] == 0.0)
+
+
+def test_cpqr_equals_qr_mode_on_full_rank():
+    """Full-rank A: both Step-2 modes precondition the same problem and converge
+    to its unique least-squares solution."""
+    A, b, SA, Sb = problem(seed=13)
+    x1, i1 = lls.solve(A, b, SA, Sb, tau_a=0.0, tau_r=1e-15, it_max=500)
+    x2, i2 = lls.solve(A, b, SA, Sb, tau_a=0.0, tau_r=1e-15, it_max=500, rcond=1e-12)
+    assert i2["rank"] == A.shape[1]
+    assert np.linalg.norm(x1 - x2) <= 1e-8 * np.linalg.norm(x1)
+
+
+def test_cpqr_rcond_truncates_small_diagonals():
+    """rcond above the smallest |r~_qq| drops exactly the trailing pivots below it."""
+    A, b, SA, Sb = problem(seed=14, cond=1e8)
+    Q, R, piv = __import__("scipy.linalg").linalg.qr(SA, mode="economic", pivoting=True)
+    dg = np.abs(np.diag(R))
+    rc = float(np.sqrt(dg[-3] * dg[-2]))  # between the 3rd- and 2nd-last
+    assert lls.cpqr_sketch(SA, rc)[3] == len(dg) - 2

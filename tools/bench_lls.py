@@ -24,7 +24,8 @@ if cm:
 else:
     A = device.dense(cfg)
     SA, Sb = skh.RhtDense(cfg.n, cfg.m, cfg.s, cfg.d)(cfg.seed, A, b)
-solver = skh.LlsSolver(cfg.n, cfg.d, cfg.m)
+rr = len(sys.argv) > 3 and sys.argv[3] == "rr"
+solver = skh.LlsSolver(cfg.n, cfg.d, cfg.m, rcond=1e-12 if rr else None)
 solver(A, b, SA, Sb, colmajor=cm)  # warm-up (handles, cuSOLVER workspace)
 torch.cuda.synchronize()
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
