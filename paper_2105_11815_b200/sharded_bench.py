@@ -21,6 +21,46 @@ def _stage_events(names, torch):
     return evs
 
 
+def comm_sweep(torch, dist, backend, sizes, iters=5):
+    """In-run collective roofline: all_to_all_single and
+    reduce_scatter_tensor at the message sizes the sharded step uses (bytes per
+    rank), timed with CUDA events on every rank (max over ranks).  Bus
+    bandwidth = bytes per rank x (G-1)/G / time, NCCL's convention for both."""
+    G = dist.get_world_size()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out = []
+    for op, nbytes in sizes:
+        n = max(G, (int(nbytes) // 8) // G * G)
+        x = torch.randn(n, dtype=torch.float64, device=dev)
+        y = torch.empty(n if op == "all_to_all" else n // G, dtype=torch.float64, device=dev)
+        if backend == "gloo":
+            x, y = x.cpu(), y.cpu()
+
+        def once():
+            if op == "all_to_all":
+                dist.all_to_all_single(y, x)
+            else:
+                dist.reduce_scatter_tensor(y, x) if backend != "gloo" else dist.all_reduce(x)
+        for _ in range(2):
+            once()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            once()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / iters], dtype=torch.float64,
+                         device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        bus = n * 8 * (G - 1) / G / (ms / 1e3) / 1e9
+        out.append({"op": op if backend != "gloo" or op == "all_to_all" else "all_reduce (gloo)",
+                    "bytes_per_rank": n * 8, "ms": round(ms, 4), "busbw_GBps": round(bus, 1)})
+    return out
+
+
 def run(args, cfg):
     import torch
     import torch.distributed as dist
@@ -144,6 +184,15 @@ def run(args, cfg):
                "steps": args.e2e_steps, "h2d_bytes_per_step": int(red_sum(A_h.numel() * 8 + b_h.numel() * 8)),
                "d2h_bytes_per_step": int(red_sum(out_bytes)), "api": type(step).__name__ + ".run (pinned shard)"}
 
+    # ---- collective roofline at the step's message sizes (all ranks take part)
+    msg = []
+    if cfg.hd and G > 1 and not isinstance(step, sharded.ShardedHrhtM3):
+        # one column chunk of the butterfly exchange: the L x W send buffer of a rank
+        msg.append(("all_to_all", (cfg.n // G) * min(cfg.d, getattr(step, "W", cfg.d)) * 8))
+    if G > 1 and cfg.kind != "csr":
+        msg.append(("reduce_scatter", ((cfg.m + G - 1) // G) * G * cfg.d * 8))
+    sweep = comm_sweep(torch, dist, backend, msg) if msg else []
+
     if rank == 0:
         from bench import METRIC, peaks
         pk, src = peaks()
@@ -197,6 +246,12 @@ def run(args, cfg):
                             "overlapped_with": "compute of the neighbouring column chunks",
                             "pipeline_ms": round(t, 4), "peer_peak_GBps": 770.0,
                             "peak_source": "B200_PROFILING.md measured peer copy"}
+        line.setdefault("comm", {})["measured"] = sweep
+        line["comm"]["backend"] = backend
+        if backend != "nccl":
+            line["comm"]["note"] = "gloo: host-staged collectives (functional run), not NVLink"
+        line["comm"].pop("peer_peak_GBps", None)
+        line["comm"].pop("peak_source", None)
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
