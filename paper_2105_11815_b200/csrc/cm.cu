@@ -39,6 +39,7 @@ namespace skh {
 namespace {
 
 constexpr int kP1Bits = 13;            // pass-1 tile: 2^13 contiguous rows (64 KiB)
+constexpr int kP1Ring = 3;             // persistent pass 1: chunks in the shared-memory ring
 constexpr int kLE = 12;                // pass-2 tile: 4096 positions per column
 constexpr int kE = 1 << kLE;
 
@@ -158,16 +159,17 @@ __global__ void __launch_bounds__(256, 3)
 
 // Persistent pass 1 for full chunks (nvalid covers every chunk, 16-byte
 // aligned columns): one CTA per SM walks chunks blockIdx.x, + gridDim.x, ...;
-// the next chunk is copied by cp.async straight into the other half of a
-// two-chunk shared-memory buffer (already in the swizzled exchange layout)
-// while this chunk's butterflies run in place in its half, so HBM reads stay
-// in flight across the compute.  Same stages, same order as cm_pass1_kernel.
+// the next kP1Ring - 1 chunks are copied by cp.async straight into the other
+// slots of a chunk ring in shared memory (already in the swizzled exchange
+// layout) while this chunk's butterflies run in place in its slot, so HBM
+// reads stay in flight across the compute.  Same stages, same order as
+// cm_pass1_kernel.
 template <bool DIAG>
 __global__ void __launch_bounds__(256, 1)
     cm_pass1p_kernel(const double* __restrict__ X, int64_t ldx, int64_t ncolX, const double* __restrict__ xb,
                      double* __restrict__ Y, int64_t ldy, int64_t nchunks, int64_t total, uint64_t dkey,
                      int64_t row0) {
-  extern __shared__ __align__(16) double2 smp[];  // [2][4096], swizzled
+  extern __shared__ __align__(16) double2 smp[];  // [kP1Ring][4096], swizzled
   const int t = threadIdx.x;
   auto issue = [&](int64_t item, int half) {
     const int64_t c = item / nchunks;
@@ -182,17 +184,18 @@ __global__ void __launch_bounds__(256, 1)
     asm volatile("cp.async.commit_group;\n" ::);
   };
   int64_t item = blockIdx.x;
-  if (item < total) issue(item, 0);
+#pragma unroll
+  for (int r = 0; r < kP1Ring - 1; ++r) {  // prologue: the first kP1Ring - 1 chunks in flight
+    if (item + (int64_t)r * gridDim.x < total) issue(item + (int64_t)r * gridDim.x, r);
+    else asm volatile("cp.async.commit_group;\n" ::);  // empty group: keeps the group count uniform
+  }
   for (int i = 0; item < total; item += gridDim.x, ++i) {
-    const int half = i & 1;
-    __syncthreads();  // every read of the other half (the previous chunk) is done
-    const int64_t next = item + gridDim.x;
-    if (next < total) {
-      issue(next, half ^ 1);
-      asm volatile("cp.async.wait_group 1;\n" ::);
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-    }
+    const int half = i % kP1Ring;
+    __syncthreads();  // every read of the slot being refilled (chunk i - 1) is done
+    const int64_t ahead = item + (int64_t)(kP1Ring - 1) * gridDim.x;
+    if (ahead < total) issue(ahead, (i + kP1Ring - 1) % kP1Ring);
+    else asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kP1Ring - 1));
     __syncthreads();  // this chunk has landed
     double2* sm = smp + half * 4096;
     const int64_t c = item / nchunks;
@@ -848,7 +851,7 @@ int launch_cm_pass1(uint64_t seed, const double* X, int64_t ldx, int64_t ncolX, 
                      reinterpret_cast<uintptr_t>(Y)) % 16 == 0) &&
                    (ldx % 2 == 0 || ncolX <= 1) && (ldy % 2 == 0);
   if (vec && nvalid >= ((int64_t)1 << L)) {  // every chunk full: the persistent double-buffered kernel
-    const size_t smem = 2 * 65536;
+    const size_t smem = (size_t)kP1Ring * 65536;
     const int64_t total = grid;
     const int64_t g = std::min<int64_t>(total, (int64_t)num_sms());
     int rc = apply_diag ? set_smem(cm_pass1p_kernel<true>, smem) : set_smem(cm_pass1p_kernel<false>, smem);
