@@ -309,6 +309,21 @@ struct Geo {
   }
 };
 
+// Geo<K2>::pf for a runtime K2 (the plan kernel serves every pass width)
+__device__ __forceinline__ int pf_rt(int K2, int t, int v) {
+  switch (K2) {
+    case 0: return Geo<0>::pf(t, v);
+    case 1: return Geo<1>::pf(t, v);
+    case 2: return Geo<2>::pf(t, v);
+    case 3: return Geo<3>::pf(t, v);
+    case 4: return Geo<4>::pf(t, v);
+    case 5: return Geo<5>::pf(t, v);
+    case 6: return Geo<6>::pf(t, v);
+    case 7: return Geo<7>::pf(t, v);
+    default: return Geo<8>::pf(t, v);
+  }
+}
+
 template <int K2>
 __device__ __forceinline__ void phase0_stages(double (&x)[16]) {
   constexpr int KR = Geo<K2>::KR, VJ = Geo<K2>::VJ;
@@ -353,6 +368,7 @@ struct PassArgs {
   int64_t ldy;
   const uint32_t* words;  // gather: [ntiles][plan_jcap(s)][kNC] owner plan words
   const int32_t* hdr;     // gather: [ntiles] steps J of the tile (< 0: serial list of -J words)
+  const uint64_t* pbank;  // gather: [ntiles][kNP] staging bank of each producer value (4 bits per register)
   int s;
   int b0, nb;             // buckets [b0, b0 + nb) accumulated by this launch
   double* SA;             // output column c < ncolSA at SA + c ldsa, column ncolSA at Sb
@@ -490,16 +506,24 @@ __global__ void __launch_bounds__(kNP + kNC, 1) cm_gather_kernel(const PassArgs 
     const int t = tid;
     double x[16], xn[16];
     int64_t ncol = blockIdx.x, ntt = 0;  // the item whose loads are in flight
-    if (nitems > 0) load_tile<K2>(a, ncol, ntt, t, xn);
+    uint64_t pbn = 0;
+    if (nitems > 0) {
+      load_tile<K2>(a, ncol, ntt, t, xn);
+      pbn = __ldg(a.pbank + ntt * kNP + t);
+    }
     for (int64_t i = 0; i < nitems; ++i) {
       const int b = (int)(i % kNBuf);
+      const uint64_t pb = pbn;
 #pragma unroll
       for (int v = 0; v < 16; ++v) x[v] = xn[v];
       if (++ntt == a.ntiles) {
         ntt = 0;
         ncol += gridDim.x;
       }
-      if (i + 1 < nitems) load_tile<K2>(a, ncol, ntt, t, xn);
+      if (i + 1 < nitems) {
+        load_tile<K2>(a, ncol, ntt, t, xn);
+        pbn = __ldg(a.pbank + ntt * kNP + t);
+      }
       phase0_stages<K2>(x);
       if (i >= kNBuf) nbar_sync(kBarEmpty + b, NALL);  // the consumers are done with buffer b
       double* ex = buf + (size_t)b * kE;
@@ -512,8 +536,11 @@ __global__ void __launch_bounds__(kNP + kNC, 1) cm_gather_kernel(const PassArgs 
         phase1_stages<K2>(x);
         nbar_sync(kBarProd, kNP);  // exchange reads done before the final values overwrite it
       }
+      // final values into the staging rows: store v of half-warp t / 16 fills row
+      // 16 v + t / 16, each lane in the bank the plan chose (a permutation per
+      // row), so that these stores and the consumers' reads are conflict-free
 #pragma unroll
-      for (int v = 0; v < 16; ++v) ex[Geo<K2>::pf(t, v)] = x[v];
+      for (int v = 0; v < 16; ++v) ex[16 * (16 * v + (t >> 4)) + (int)((pb >> (4 * v)) & 15u)] = x[v];
       nbar_arrive(kBarFull + b, NALL);
     }
     return;
@@ -638,9 +665,12 @@ __device__ __forceinline__ int block_excl_scan_256(int v, int* tmp, int& total) 
 __global__ void __launch_bounds__(256) cm_plan_kernel(const int32_t* __restrict__ col_rows,
                                                       const int8_t* __restrict__ col_signs, int s, int K2, int lo,
                                                       int64_t nvalid, int b0, int nb, uint32_t* __restrict__ words,
-                                                      int32_t* __restrict__ hdr) {
+                                                      int32_t* __restrict__ hdr, uint64_t* __restrict__ pbank) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int tmp[16];
+  __shared__ uint8_t gpos[kE];     // staging row (producer store group) of position p
+  __shared__ int bnk[kE];          // its bank in that row (0xFF: not chosen yet)
+  __shared__ unsigned avail[256];  // banks still free per row
   __shared__ int bnd[16][17];
   __shared__ int cstart[17];
   __shared__ int jmax;
@@ -653,6 +683,12 @@ __global__ void __launch_bounds__(256) cm_plan_kernel(const int32_t* __restrict_
   int* off = reinterpret_cast<int*>(smraw + sizeof(uint32_t) * E);  // [no]
   for (int o = tid; o < no; o += 256) off[o] = 0;
   if (tid == 0) jmax = 0;
+  for (int v = 0; v < 16; ++v) {  // producer thread tid stores its register v as row 16 v + tid / 16
+    const int p = pf_rt(K2, tid, v);
+    gpos[p] = (uint8_t)(16 * v + (tid >> 4));
+    bnk[p] = 0xFF;
+  }
+  avail[tid] = 0xFFFFu;
   __syncthreads();
   auto entry = [&](int e, int& k, int& neg) {  // local bucket of entry e (-1: none in this launch)
     const int p = e / s, q = e - p * s;
@@ -728,33 +764,84 @@ __global__ void __launch_bounds__(256) cm_plan_kernel(const int32_t* __restrict_
   __syncthreads();
   const int J8 = (jmax + 3) & ~3;  // steps: a multiple of 4 (one uint4 of words)
   uint32_t* out = words + tt * plan_tile_words(s);
+  // claim a free bank of row g for position p (unique per row), preferring the
+  // banks in `want`; returns the bank
+  // (s = 1: every position is claimed once, and a row never has more claims
+  // than its 16 banks)
+  auto claim = [&](int p, unsigned want) {
+    const int g = gpos[p];
+    for (;;) {
+      const unsigned av = *(volatile unsigned*)&avail[g];
+      unsigned m = av & want;
+      if (!m) m = av;
+      const int b = __ffs(m) - 1;
+      if ((atomicAnd(&avail[g], ~(1u << b)) >> b) & 1u) {
+        bnk[p] = b;
+        return b;
+      }
+    }
+  };
+  auto slot_of = [&](int p) { return 16 * (int)gpos[p] + (int)bnk[p]; };
+  // the staging colouring is built for s = 1 (one entry per position: each
+  // position claims one bank of its row once); s > 1 and serial tiles keep the
+  // natural banks (bank = producer lane)
+  const bool colour = s == 1 && J8 <= plan_jcap(s);
+  if (!colour) {
+    for (int v = 0; v < 16; ++v) bnk[pf_rt(K2, tid, v)] = tid & 15;
+    __syncthreads();
+  }
   if (J8 > plan_jcap(s)) {  // serial list in ascending e
     for (int e = tid; e < E; e += 256) {
       int k, neg;
       entry(e, k, neg);
-      out[e] = k < 0 ? 0u : ((uint32_t)(e / s) | ((uint32_t)k << 12) | kValid | ((uint32_t)neg << 31));
+      out[e] = k < 0 ? 0u : ((uint32_t)slot_of(e / s) | ((uint32_t)k << 12) | kValid | ((uint32_t)neg << 31));
     }
+    uint64_t pb = 0;
+    for (int v = 0; v < 16; ++v) pb |= (uint64_t)(tid & 15) << (4 * v);
+    pbank[tt * kNP + tid] = pb;
     if (tid == 0) hdr[tt] = -E;
     return;
   }
   // (5) words: the thread's runs in order, each run's entries in ascending e,
-  // flagged head (first of its bucket) and last.  (Ordering the runs per step so
-  // the 16 lanes of a half-warp read distinct banks of the staged tile was
-  // measured: a greedy leaves ~1.95 wavefronts per half-warp step -- the lanes
-  // run out of candidates -- for -4 % of the pass at 10x the plan time.)
+  // flagged head (first of its bucket) and last.  (Reordering the runs per step
+  // so a half-warp reads distinct banks was measured: a greedy leaves ~1.95
+  // wavefronts per half-warp step.)  Instead the STAGING LAYOUT is coloured: a
+  // position's slot is (producer store row, bank) and, step by step, the 16
+  // lanes of a consumer half-warp claim distinct banks, each from the free banks
+  // of its position's row -- a bipartite edge colouring (rows x half-warp steps,
+  // 16 colours, which exists by Konig's theorem); the greedy claim falls back to
+  // any free bank of the row, a rare 2-way conflict.
   const uint32_t* mine = sorted + cs + i0;
   const int c = 32 * (u >> 1) + 16 * (u & 1) + cl;  // consumer thread of (class cl, slot u)
   for (int j = 0; j < J8; ++j) {
     uint32_t wd = 0;
+    int p = -1;
     if (j < cnt) {
       const uint32_t x = mine[j];
       const uint32_t kb = (x >> 15) & 0xFFFFu;
       const bool head = j == 0 || ((mine[j - 1] >> 15) & 0xFFFFu) != kb;
       const bool last = j + 1 == cnt || ((mine[j + 1] >> 15) & 0xFFFFu) != kb;
-      wd = (uint32_t)((x & 0x7FFFu) / s) | (kb << 12) | (x & 0x80000000u) | (head ? kHead : 0u) | (last ? kLast : 0u);
+      p = (int)(x & 0x7FFFu) / s;
+      wd = (kb << 12) | (x & 0x80000000u) | (head ? kHead : 0u) | (last ? kLast : 0u);
     }
+    if (colour) {
+      unsigned used = 0;  // banks taken by the lanes before, this step, this half-warp
+      for (int L = 0; L < 16; ++L) {
+        if (cl == L && p >= 0) used |= 1u << claim(p, ~used);
+        used = __shfl_sync(0xffffffffu, used, (tid & 16) + L);
+      }
+    }
+    if (p >= 0) wd |= (uint32_t)slot_of(p);
     out[plan_index(j, c)] = wd;
   }
+  __syncthreads();
+  if (colour)
+    for (int p = tid; p < kE; p += 256)  // positions no entry reads: any free bank of their row
+      if (bnk[p] == 0xFF) claim(p, 0xFFFFu);
+  __syncthreads();
+  uint64_t pb = 0;  // producer thread tid's banks, 4 bits per register
+  for (int v = 0; v < 16; ++v) pb |= (uint64_t)bnk[pf_rt(K2, tid, v)] << (4 * v);
+  pbank[tt * kNP + tid] = pb;
   if (tid == 0) hdr[tt] = J8;
 }
 
@@ -812,7 +899,15 @@ int launch_gather_t(const PassArgs& a, cudaStream_t st) {
 
 size_t plan_range_bytes(int64_t ntiles, int s) {
   return align_up(sizeof(uint32_t) * (size_t)ntiles * (size_t)plan_tile_words(s)) +
-         align_up(sizeof(int32_t) * (size_t)ntiles);
+         align_up(sizeof(int32_t) * (size_t)ntiles) + align_up(sizeof(uint64_t) * (size_t)ntiles * kNP);
+}
+// [words][hdr][pbank] of one bucket range
+const int32_t* plan_hdr(const char* base, int64_t ntiles, int s) {
+  return reinterpret_cast<const int32_t*>(base + align_up(sizeof(uint32_t) * (size_t)ntiles * plan_tile_words(s)));
+}
+const uint64_t* plan_pbank(const char* base, int64_t ntiles, int s) {
+  return reinterpret_cast<const uint64_t*>(base + align_up(sizeof(uint32_t) * (size_t)ntiles * plan_tile_words(s)) +
+                                           align_up(sizeof(int32_t) * (size_t)ntiles));
 }
 
 }  // namespace
@@ -822,7 +917,7 @@ size_t plan_range_bytes(int64_t ntiles, int s) {
 int cm_max_buckets(int s) {
   if (s < 1 || s > 8) return 0;
   const size_t avail = 227 * 1024 - (size_t)kNBuf * kE * 8;                // gather: staged tiles + SA
-  const size_t avail_plan = 227 * 1024 - (size_t)4 * kE * s - 16;           // plan: entries + counters
+  const size_t avail_plan = 227 * 1024 - (size_t)4 * kE * s - 16 - 24 * 1024;  // plan: entries, counters, colouring
   return (int)(std::min(avail / 8, avail_plan / 4) & ~(size_t)15);
 }
 
@@ -927,12 +1022,18 @@ int launch_cm_lists(const int32_t* col_rows, const int8_t* col_signs, int s, int
   for (int64_t b0 = 0; b0 < m; b0 += cap) {
     const int nb = (int)std::min<int64_t>(cap, m - b0);
     uint32_t* words = reinterpret_cast<uint32_t*>(base);
-    int32_t* hdr = reinterpret_cast<int32_t*>(base + align_up(sizeof(uint32_t) * (size_t)ntiles * plan_tile_words(s)));
+    int32_t* hdr = const_cast<int32_t*>(plan_hdr(base, ntiles, s));
+    uint64_t* pbank = const_cast<uint64_t*>(plan_pbank(base, ntiles, s));
     const size_t smem = plan_smem_bytes(s, nb);
-    int rc = set_smem(cm_plan_kernel, smem);
-    if (rc) return rc;
+    // the kernel also holds ~22 KB of static shared memory (the staging colouring)
+    if (cudaFuncSetAttribute(cm_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("cm plan: %zu bytes of shared memory", smem);
+      return SKH_ECUDA;
+    }
+    int rc;
     cm_plan_kernel<<<(unsigned)ntiles, 256, smem, st>>>(col_rows, col_signs, s, K2, lo, nvalid, (int)b0, nb, words,
-                                                         hdr);
+                                                         hdr, pbank);
     note_launch();
     if ((rc = check_launch("cm_plan"))) return rc;
     base += plan_range_bytes(ntiles, s);
@@ -970,7 +1071,8 @@ int launch_cm_gather(const double* X, int64_t ldx, int64_t ncolX, const double* 
     a.b0 = (int)b0;
     a.nb = (int)std::min<int64_t>(cap, m - b0);
     a.words = reinterpret_cast<const uint32_t*>(base);
-    a.hdr = reinterpret_cast<const int32_t*>(base + align_up(sizeof(uint32_t) * (size_t)ntiles * plan_tile_words(s)));
+    a.hdr = plan_hdr(base, ntiles, s);
+    a.pbank = plan_pbank(base, ntiles, s);
     int rc;
     switch (K2) {
       case 0: rc = launch_gather_t<0>(a, st); break;
