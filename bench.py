@@ -260,10 +260,17 @@ def kernel_table(cfg, step, layout, sketch):
         return {"gather_csr": ("csr_expand + csr_reduce", cfg.a_bytes + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5, 1)}
     if cfg.hd:
         t = {f"fwht_pass{p}": (f"fwht_tile_kernel<{k}>", step.n_pad * cfg.d * 8, 1) for p, k in enumerate(step.plan)}
-        t["gather"] = ("gather_wide_kernel", step.n_pad * cfg.d * 8 + cfg.m * cfg.d * 8 + step.n_pad * cfg.s * 5, 1)
+        t["gather"] = (gather_kernel_name(cfg), step.n_pad * cfg.d * 8 + cfg.m * cfg.d * 8 + step.n_pad * cfg.s * 5, 1)
         return t
-    name = "gather_wide_kernel" if (cfg.d % 2 == 0 and cfg.d > 64) else "gather_dense_kernel"
+    name = gather_kernel_name(cfg)
     return {"gather": (name, cfg.n * cfg.d * 8 + cfg.m * cfg.d * 8 + cfg.n * cfg.s * 5, 1)}
+
+
+def gather_kernel_name(cfg):
+    """The dense gather the library launches for this shape (csrc/gather.cu)."""
+    if cfg.d % 2 == 0 and cfg.d > 64:
+        return "gather_group_kernel<16>" if cfg.s > 1 else "gather_wide_kernel"
+    return "gather_dense_kernel"
 
 
 def traffic_record(cfg, layout):

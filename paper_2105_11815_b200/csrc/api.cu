@@ -243,7 +243,7 @@ int rht_tail(uint64_t seed, int64_t n, int64_t n_pad, int L, int64_t m, int s, i
   }
   (void)K0;
   const double c = skh_c_ns(n_pad, s);
-  rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.Y, d, SA, ldsa, c, st);
+  rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.Y, d, SA, ldsa, c, st, s);
   if (rc) return rc;
   if (b_dev) {
     rc = launch_fwht(seed, n_pad, n, 0, 1, b_dev, 1, w.yb, 1, 0, L, 1, 1.0, w.dw, st);
@@ -353,7 +353,7 @@ int skh_sketch_dense(int64_t m, int32_t s, const int32_t* bucket_ptr, const int3
   // Sb (latency-bound, one warp per bucket) on the side stream beside S A
   cudaStream_t side = b ? side_fork(st) : st;
   if (b) rc = launch_gather_vec(m, bucket_ptr, bucket_rows, bucket_signs, b, Sb, alpha, side);
-  if (!rc) rc = launch_gather_dense(m, bucket_ptr, bucket_rows, bucket_signs, d, A, lda, SA, ldsa, alpha, st);
+  if (!rc) rc = launch_gather_dense(m, bucket_ptr, bucket_rows, bucket_signs, d, A, lda, SA, ldsa, alpha, st, s);
   // join on every path after the fork: the caller's stream stays ordered after the side work
   const int jc = b ? side_join(st, side) : SKH_OK;
   return rc ? rc : jc;
@@ -467,7 +467,7 @@ int skh_rht_dense(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, con
   const bool fast = fwht_fast_ok(w.Y, d, w.Y, d, d);
   // all passes done by launch_fwht: run only the gather part of the tail
   const double c = skh_c_ns(n_pad, s);
-  rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.Y, d, SA, ldsa, c, st);
+  rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.Y, d, SA, ldsa, c, st, s);
   if (rc) return rc;
   (void)fast;
   if (b) {
@@ -594,7 +594,7 @@ int skh_sketch_dense_host(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_
   cudaEventRecord(ev, cs);
   cudaStreamWaitEvent(st, ev, 0);
   const double c = skh_c_s(s);
-  if (!rc) rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.X, d, w.SA, d, c, st);
+  if (!rc) rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.X, d, w.SA, d, c, st, s);
   if (!rc && b_host) rc = launch_gather_vec(m, w.ptr, w.rows, w.signs, w.bin, w.Sb, c, st);
   if (!rc && cudaMemcpy2DAsync(SA_host, sizeof(double) * ldsa, w.SA, sizeof(double) * d, sizeof(double) * d, m,
                                cudaMemcpyDeviceToHost, st) != cudaSuccess)

@@ -370,7 +370,7 @@ int skh_sketch_dense_colmajor(uint64_t seed, int64_t n, int64_t m, int32_t s, in
     if ((rc = check_launch("sketch_dense_colmajor: transpose"))) return rc;
     skh_trace_mark(st, "transpose");
     const double c = skh_c_s(s);
-    if ((rc = launch_gather_dense(m, f.ptr, f.rows, f.signs, d, f.Arm, d, f.SAt, d, c, st))) return rc;
+    if ((rc = launch_gather_dense(m, f.ptr, f.rows, f.signs, d, f.Arm, d, f.SAt, d, c, st, s))) return rc;
     if (b && (rc = launch_gather_vec(m, f.ptr, f.rows, f.signs, b, Sb, c, st))) return rc;
     transpose_cm_to_rm(d, m, f.SAt, d, SA, ldsa, st);
     if ((rc = check_launch("sketch_dense_colmajor: SA transpose"))) return rc;

@@ -64,9 +64,11 @@ int hash_status(const void* ws, cudaStream_t st);
 int64_t scan_scratch_ints(int64_t len);
 int launch_excl_scan_i32(int32_t* a, int64_t len, int32_t* blocksums, cudaStream_t st);
 // gather.cu
+// s = nonzeros per row of S (the number of reads of each row): s > 1 takes the
+// L2-slice lane-group kernel, s = 1 the 128-column wide kernel
 int launch_gather_dense(int64_t m, const int32_t* ptr, const int32_t* rows, const int8_t* sg,
                         int64_t d, const double* A, int64_t lda, double* SA, int64_t ldsa,
-                        double alpha, cudaStream_t st);
+                        double alpha, cudaStream_t st, int s = 2);
 int launch_gather_vec(int64_t m, const int32_t* ptr, const int32_t* rows, const int8_t* sg,
                       const double* b, double* Sb, double alpha, cudaStream_t st);
 // csr.cu

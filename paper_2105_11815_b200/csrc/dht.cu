@@ -359,7 +359,7 @@ int hrdht_run(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const d
     if ((rc = check_launch("hrdht: transpose"))) return rc;
     skh_trace_mark(st, "transpose");
     if ((rc = launch_dht_pow2(n, d, w.H, d, b, dkey, (double2*)w.Z, (double2*)w.tw, w.H, d, w.hb, st))) return rc;
-    if ((rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.H, d, w.SAt, d, c, st))) return rc;
+    if ((rc = launch_gather_dense(m, w.ptr, w.rows, w.signs, d, w.H, d, w.SAt, d, c, st, s))) return rc;
     if (b && (rc = launch_gather_vec(m, w.ptr, w.rows, w.signs, w.hb, Sb, c, st))) return rc;
     transpose_cm_to_rm(d, m, w.SAt, d, SA, ldsa, st);  // SA[c * ldsa + b] = SAt[b * d + c]
     if ((rc = check_launch("hrdht: SA transpose"))) return rc;

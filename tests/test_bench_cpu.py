@@ -61,7 +61,7 @@ def test_roofline_gather_csr_and_dht():
     c3 = cfg_of("C3")
     r = b.roofline(c3, None, {"hash_gen": 0.06, "gather": 0.95}, 1.01, PEAK, "test")
     check(r, c3.n * c3.d * 8 + c3.m * c3.d * 8 + c3.n * c3.s * 5, 0.95, c3, 1.01, c3.n)
-    assert r["kernel"] == "gather_wide_kernel"
+    assert r["kernel"] == "gather_group_kernel<16>"  # s = 2: the L2-slice kernel
     c4 = cfg_of("C4")
     r = b.roofline(c4, None, {"hash_gen": 0.14, "gather_csr": 0.57}, 0.72, PEAK, "test")
     check(r, c4.n * c4.nnz_row * 12 + (c4.n + 1) * 8 + c4.m * c4.d * 8 + c4.n * c4.s * 5, 0.57, c4, 0.72, c4.n)

@@ -15,8 +15,8 @@ STAGES = {
     "C2-row": {"fwht_pass0": ["fwht_tile_kernel<8, 1>"], "fwht_pass1": ["fwht_tile_kernel<8, 0>"],
                "gather": ["gather_wide_kernel"]},
     "C3HD-row": {"fwht_pass0": ["fwht_tile_kernel<9, 1>"], "fwht_pass1": ["fwht_tile_kernel<8, 0>"],
-                 "gather": ["gather_wide_kernel"]},
-    "C3-row": {"gather": ["gather_wide_kernel"]},
+                 "gather": ["gather_group_kernel"]},
+    "C3-row": {"gather": ["gather_group_kernel"]},
     "C4-row": {"gather_csr": ["csr_len_kernel", "csr_expand_kernel", "csr_reduce_kernel"]},
 }
 FILES = {"C5-col": "C5_auto", "C5-row": "C5_row", "C2-row": "C2_auto", "C3HD-row": "C3HD_auto", "C3-row": "C3_auto",
