@@ -324,13 +324,15 @@ def default_layout(cfg):
     """Storage of dense A the bench times by default: column-major (the paper's
     LAPACK/FFTW layout) for an H D workload whose row-major transform
     needs >= 3 HBM passes -- there the two-pass column-major plan (pass 2 fused
-    with the sketch) moves 3|A| instead of 7|A| and wins (C5) -- else
-    row-major (C2, C3HD: two row passes; plain sketches: one read)."""
+    with the sketch) moves 3|A| instead of 7|A| and wins (C5) -- or whose hash is
+    s = 1 (C2: the column-major step, hash + tile lists beside pass 1, 0.44 ms vs
+    0.50 row-major); else row-major (C3HD, s = 2: 3.69 vs 3.84 ms; plain
+    sketches: one read)."""
     if not cfg.hd or cfg.kind == "csr":
         return "row"
     from paper_2105_11815_b200 import api
     n_pad = 1 << max(0, (cfg.n - 1).bit_length())
-    return "col" if len(api.rht_pass_plan(n_pad.bit_length() - 1, cfg.d)) >= 3 else "row"
+    return "col" if (len(api.rht_pass_plan(n_pad.bit_length() - 1, cfg.d)) >= 3 or cfg.s == 1) else "row"
 
 
 def freivalds_check(cfg, SA, inputs, layout, nprobe=4):

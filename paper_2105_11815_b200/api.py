@@ -410,10 +410,17 @@ class Trace:
         return False
 
     def durations_ms(self):
-        """{stage: ms} of the last traced call (synchronize first)."""
+        """{stage: ms} of the last traced call (synchronize first).  Stages the
+        library ran on its side stream (trace names "side:...") form their own
+        chain from the first event and are reported as "<stage> (overlapped)",
+        outside the main-stream sum."""
         out = {}
+        prev = {False: 0, True: 0}
         for i in range(1, self.count):
-            out[self.names[i]] = out.get(self.names[i], 0.0) + self.events[i - 1].elapsed_time(self.events[i])
+            side = self.names[i].startswith("side:")
+            name = self.names[i][5:] + " (overlapped)" if side else self.names[i]
+            out[name] = out.get(name, 0.0) + self.events[prev[side]].elapsed_time(self.events[i])
+            prev[side] = i
         return out
 
 

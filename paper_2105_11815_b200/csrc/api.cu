@@ -256,6 +256,9 @@ int rht_tail(uint64_t seed, int64_t n, int64_t n_pad, int L, int64_t m, int s, i
 
 }  // namespace
 
+cudaStream_t skh_side_fork(cudaStream_t st) { return side_fork(st); }
+int skh_side_join(cudaStream_t st, cudaStream_t side) { return side_join(st, side); }
+
 cudaStream_t skh_copy_stream() { return copy_stream(); }
 
 }  // namespace skh

@@ -4,6 +4,7 @@
 // skh_rht_colmajor; plus the stage-trace hook (skh_trace_*).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -14,7 +15,8 @@ namespace skh {
 // cm.cu
 int cm_max_buckets(int s);
 int launch_cm_pass1(uint64_t seed, const double* X, int64_t ldx, int64_t ncolX, const double* xb, double* Y,
-                    int64_t ldy, int64_t nvalid, int L, int apply_diag, int64_t row0, cudaStream_t st);
+                    int64_t ldy, int64_t nvalid, int L, int apply_diag, int64_t row0, cudaStream_t st,
+                    int reserve_sms = 0);
 int launch_cm_mid(double* Y, int64_t ldy, int64_t ncols, int64_t nrows, int lo, int K2, cudaStream_t st);
 size_t cm_lists_bytes(int64_t ntiles, int s, int64_t m);
 int launch_cm_lists(const int32_t* col_rows, const int8_t* col_signs, int s, int64_t m, int K2, int lo,
@@ -133,17 +135,33 @@ CmWs cm_layout(void* base, int64_t nrows_hash, int64_t ycols, int64_t yrows, int
   return w;
 }
 
-// Hash + tile lists (R1, R2 in tile order).
+// Hash + tile lists (R1, R2 in tile order).  side: on the side stream (trace
+// names "side:...", timed from the fork)
 int cm_prepare(uint64_t seed, int64_t nrows_hash, int64_t m, int s, const CmPlan& pl, const CmWs& w,
-               cudaStream_t st) {
+               cudaStream_t st, bool side = false) {
   int rc = launch_hash(seed, m, s, nrows_hash, 0, 0, 0, w.col_rows, w.col_signs, w.ptr, w.rows, w.signs, w.hws,
                        hash_ws_bytes(nrows_hash, m, s), st);
   if (rc) return rc;
-  skh_trace_mark(st, "hash_gen");
+  skh_trace_mark(st, side ? "side:hash_gen" : "hash_gen");
   rc = launch_cm_lists(w.col_rows, w.col_signs, s, m, pl.K2, pl.lo2, nrows_hash, pl.ntiles, w.lists, st);
   if (rc) return rc;
-  skh_trace_mark(st, "tile_lists");
+  skh_trace_mark(st, side ? "side:tile_lists" : "tile_lists");
   return SKH_OK;
+}
+
+// SMs pass 1 leaves to the side stream's tile-list kernel (one CTA per tile,
+// which cannot share an SM with a pass-1 CTA): only where the hash + lists are a
+// sizeable share of pass 1, because pass 1 slows in proportion to the SMs it
+// loses (measured, C2 / C3HD / C5 total ms: reserve 0: 0.545 / 3.840 / 44.59,
+// 8: 0.442 / 3.858 / 45.80, 16: 0.450 / 3.931 / 47.16).  SKH_CM_RESERVE overrides.
+int pass1_reserve(const CmPlan& pl, int64_t ncols) {
+  static const int env = [] {
+    const char* e = getenv("SKH_CM_RESERVE");
+    return e ? atoi(e) : -1;
+  }();
+  if (env >= 0) return env;
+  const int64_t chunks = ncols * (((int64_t)1 << pl.L) >> kCmP1);
+  return chunks < 32768 ? (int)std::min<int64_t>(pl.ntiles, 8) : 0;
 }
 
 // Transform passes after pass 1 (mid passes) then the fused final pass.
@@ -232,11 +250,16 @@ int skh_rht_dense_colmajor(uint64_t seed, int64_t n, int64_t m, int32_t s, int64
   }
   cudaStream_t st = as_stream(stream);
   trace_begin(st);
-  rc = cm_prepare(seed, n_pad, m, s, pl, w, st);
+  // hash + tile lists depend only on (seed, n, m, s): on the side stream, beside pass 1
+  cudaStream_t ss = skh_side_fork(st);
+  rc = cm_prepare(seed, n_pad, m, s, pl, w, ss, ss != st);
+  if (!rc) rc = launch_cm_pass1(seed, A, lda, d, b, w.Y, n_pad, n, pl.L, 1, 0, st,
+                                ss != st ? pass1_reserve(pl, ncols) : 0);
+  if (!rc) skh_trace_mark(st, "pass1");
+  const int jc = skh_side_join(st, ss);  // join on every path after the fork
   if (rc) return rc;
-  rc = launch_cm_pass1(seed, A, lda, d, b, w.Y, n_pad, n, pl.L, 1, 0, st);
-  if (rc) return rc;
-  skh_trace_mark(st, "pass1");
+  if (jc) return jc;
+  skh_trace_mark(st, "side_wait");
   return cm_rht_tail(pl, n_pad, ncols, d, m, s, w, SA, ldsa, Sb, st);
 }
 

@@ -922,8 +922,11 @@ int cm_max_buckets(int s) {
 }
 
 // Pass 1 of columns of 2^L rows: bits [0, min(L, 13)).
+// reserve_sms: SMs the persistent kernel leaves free (for side-stream work that
+// runs beside it)
 int launch_cm_pass1(uint64_t seed, const double* X, int64_t ldx, int64_t ncolX, const double* xb, double* Y,
-                    int64_t ldy, int64_t nvalid, int L, int apply_diag, int64_t row0, cudaStream_t st) {
+                    int64_t ldy, int64_t nvalid, int L, int apply_diag, int64_t row0, cudaStream_t st,
+                    int reserve_sms) {
   const int64_t ncols = ncolX + (xb ? 1 : 0);
   if (ncols == 0) return SKH_OK;
   const uint64_t dkey = key_diag(seed);
@@ -948,7 +951,7 @@ int launch_cm_pass1(uint64_t seed, const double* X, int64_t ldx, int64_t ncolX, 
   if (vec && nvalid >= ((int64_t)1 << L)) {  // every chunk full: the persistent double-buffered kernel
     const size_t smem = (size_t)kP1Ring * 65536;
     const int64_t total = grid;
-    const int64_t g = std::min<int64_t>(total, (int64_t)num_sms());
+    const int64_t g = std::min<int64_t>(total, (int64_t)std::max(1, num_sms() - std::max(0, reserve_sms)));
     int rc = apply_diag ? set_smem(cm_pass1p_kernel<true>, smem) : set_smem(cm_pass1p_kernel<false>, smem);
     if (rc) return rc;
     if (apply_diag)

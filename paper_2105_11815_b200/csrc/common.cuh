@@ -89,6 +89,9 @@ void skh_trace_mark(cudaStream_t st, const char* name);
 void skh_trace_start(cudaStream_t st);
 // api.cu: library-owned copy stream of the current device (host-buffer variants)
 cudaStream_t skh_copy_stream();
+// api.cu: per-thread side stream; fork = it waits for `st`, join = `st` waits for it
+cudaStream_t skh_side_fork(cudaStream_t st);
+int skh_side_join(cudaStream_t st, cudaStream_t side);
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 

@@ -241,9 +241,11 @@ def test_trace_stage_events():
     with skh().api.Trace(8) as tr:
         op(cfg.seed, At)
     torch.cuda.synchronize()
-    assert tr.names == ["begin", "hash_gen", "tile_lists", "pass1", "pass2_gather"]
+    # hash + tile lists run on the library's side stream beside pass 1
+    assert tr.names == ["begin", "side:hash_gen", "side:tile_lists", "pass1", "side_wait", "pass2_gather"]
     ms = tr.durations_ms()
     assert all(v >= 0 for v in ms.values())
+    assert set(ms) == {"hash_gen (overlapped)", "tile_lists (overlapped)", "pass1", "side_wait", "pass2_gather"}
 
 
 def test_determinism_stress_shared_memory_paths():
