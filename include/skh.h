@@ -253,6 +253,19 @@ int skh_scale(double* X, int64_t rows, int64_t cols, int64_t ldx, double alpha,
 int skh_fold_lists(int64_t nentries, int32_t* bucket_rows, int8_t* bucket_signs,
                    int64_t L, int64_t rank, void* stream);
 
+/* The same fold in COLUMN-list form, for the column-major M3 path (the
+ * on-chip fan-out of SURVEY §8(e) M3): given the column lists of all n = G L
+ * columns of S (skh_hash_gen col_rows / col_signs, nrows = n, row0 = 0;
+ * [n][s] row-major), writes T_r's column lists over the L local rows:
+ *   fold_rows[l (G s) + g s + q]  = col_rows[(g L + l) s + q]
+ *   fold_signs[l (G s) + g s + q] = col_signs[(g L + l) s + q] * (-1)^popcount(g & rank)
+ * for l < L, g < G, q < s (device arrays, caller-owned; fold_* hold L G s
+ * entries).  A bucket may appear twice in one local row (two blocks g hit it):
+ * the sum keeps both terms.  Errors: SKH_EINVAL (L < 1, G < 1, s < 1, rank
+ * outside [0, G), null pointers). */
+int skh_fold_cols(int64_t L, int64_t G, int32_t s, int64_t rank, const int32_t* col_rows,
+                  const int8_t* col_signs, int32_t* fold_rows, int8_t* fold_signs, void* stream);
+
 /* Deterministic ordered sum of G partial blocks laid out consecutively:
  * out[r, c] = (((P_0[r,c] + P_1[r,c]) + P_2[r,c]) + ...) * alpha, where
  * P_g = parts + g * part_stride (elements), each [rows x cols] with ld `ldp`.
@@ -284,6 +297,28 @@ size_t skh_rht_dense_colmajor_workspace_bytes(int64_t n, int64_t m, int32_t s, i
 int skh_rht_dense_colmajor(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d,
                            const double* A, int64_t lda, const double* b,
                            double* SA, int64_t ldsa, double* Sb,
+                           void* ws, size_t ws_bytes, void* stream);
+
+/* Column-major H_L D A_r and its sketch with CALLER-GIVEN column lists (the
+ * M3 rank step; P:L790-801 for H D, L871 for S_h): A is the
+ * rank's L local rows (column-major, column c at A + c lda, lda >= L), D uses
+ * global ids row0 + l, H_L is the unnormalised transform over the L rows
+ * (padded with zero rows to n_pad, the next power of two >= L), and the
+ * sketch takes s_eff entries per row of the transformed (padded) block from
+ * col_rows / col_signs ([n_pad][s_eff]: H mixes the padding rows in, so they
+ * need lists too; bucket ids in [0, m), signs +-1; e.g. skh_fold_cols' T_r
+ * lists, L a power of two, s_eff = G s <= 8).  Output
+ * column-major like skh_rht_dense_colmajor: SAt[c ldsa + k] = alpha * (the
+ * signed sum of bucket k over the transformed column c), ldsa >= m; Sb[k]
+ * likewise for b (optional, L doubles).  alpha = 1 gives the unscaled partial
+ * of the deterministic strip reduction.  Workspace:
+ * skh_rht_colmajor_lists_workspace_bytes (device, caller-owned).  Errors:
+ * SKH_EINVAL (bad sizes, s_eff > 8, null A/SAt/lists, b without Sb),
+ * SKH_EWORKSPACE, SKH_ECUDA. */
+size_t skh_rht_colmajor_lists_workspace_bytes(int64_t L, int64_t m, int32_t s_eff, int64_t d);
+int skh_rht_colmajor_lists(uint64_t seed, int64_t L, int64_t row0, int64_t m, int32_t s_eff, int64_t d,
+                           const double* A, int64_t lda, const double* b, const int32_t* col_rows,
+                           const int8_t* col_signs, double alpha, double* SAt, int64_t ldsa, double* Sb,
                            void* ws, size_t ws_bytes, void* stream);
 /* Same from HOST buffers (pinned recommended): A_host is copied in groups of
  * columns on a library copy stream, each group transformed (pass 1) as soon as

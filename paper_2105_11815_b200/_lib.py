@@ -48,6 +48,10 @@ SIGNATURES = {
     "skh_scale": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_d, c_p]),
     "skh_ordered_sum": (ctypes.c_int, [c_p, c_i64, c_i64, c_i64, c_i64, c_i64, c_p, c_i64, c_d, c_p]),
     "skh_fold_lists": (ctypes.c_int, [c_i64, c_p, c_p, c_i64, c_i64, c_p]),
+    "skh_fold_cols": (ctypes.c_int, [c_i64, c_i64, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p]),
+    "skh_rht_colmajor_lists_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32, c_i64]),
+    "skh_rht_colmajor_lists": (ctypes.c_int, [c_u64, c_i64, c_i64, c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_p, c_p,
+                                              c_d, c_p, c_i64, c_p, c_p, c_sz, c_p]),
     "skh_rht_dense_colmajor_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32, c_i64]),
     "skh_rht_dense_colmajor": (ctypes.c_int, [c_u64, c_i64, c_i64, c_i32, c_i64, c_p, c_i64, c_p, c_p, c_i64, c_p,
                                               c_p, c_sz, c_p]),

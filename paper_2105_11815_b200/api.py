@@ -297,6 +297,50 @@ def _ld_cm(t, rows):
     return t.stride(0)
 
 
+def fold_cols(col_rows, col_signs, L, G, s, rank, out=None):
+    """T_r's column lists over L local rows from the column lists of all n = G L
+    columns of S (skh_fold_cols; the column-major exchange-free sharded H D A,
+    DESIGN.md §7).  Returns (rows, signs) of L G s entries."""
+    lib = _lib.load()
+    _need_cuda(col_rows, col_signs)
+    N = int(L) * int(G) * int(s)
+    if out is None:
+        out = (torch.empty(N, dtype=torch.int32, device=col_rows.device),
+               torch.empty(N, dtype=torch.int8, device=col_rows.device))
+    _lib.check(lib.skh_fold_cols(int(L), int(G), int(s), int(rank), _ptr(col_rows), _ptr(col_signs), _ptr(out[0]),
+                                 _ptr(out[1]), _stream()), "skh_fold_cols")
+    return out
+
+
+class RhtColMajorLists:
+    """SA^T = alpha * S' H_L D A_r for a column-major local block At (d, L) with
+    caller-given column lists (s_eff per row of the transform, next power of two
+    >= L rows; skh_rht_colmajor_lists), D over global ids row0 + l.  The M3 rank
+    step; returns SA^T (d, m) and Sb."""
+
+    def __init__(self, L, m, s_eff, d, device=None):
+        lib = _lib.load()
+        self.L, self.m, self.s_eff, self.d = int(L), int(m), int(s_eff), int(d)
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        self.ws = _workspace(lib.skh_rht_colmajor_lists_workspace_bytes(L, m, s_eff, d), device)
+
+    def __call__(self, seed, At, b, row0, col_rows, col_signs, alpha=1.0, SAt=None, Sb=None):
+        lib = _lib.load()
+        _need_cuda(At, b, col_rows, col_signs)
+        if tuple(At.shape) != (self.d, self.L) or At.dtype != torch.float64:
+            raise ValueError(f"At must be float64 of shape (d, L) = ({self.d}, {self.L})")
+        if SAt is None:
+            SAt = torch.empty(self.d, self.m, dtype=torch.float64, device=At.device)
+        if b is not None and Sb is None:
+            Sb = torch.empty(self.m, dtype=torch.float64, device=At.device)
+        rc = lib.skh_rht_colmajor_lists(int(seed) & (2**64 - 1), self.L, int(row0), self.m, self.s_eff, self.d,
+                                        _ptr(At), _ld_cm(At, self.L), _ptr(b), _ptr(col_rows), _ptr(col_signs),
+                                        float(alpha), _ptr(SAt), _ld_cm(SAt, self.m), _ptr(Sb), _ptr(self.ws),
+                                        self.ws.numel(), _stream())
+        _lib.check(rc, "skh_rht_colmajor_lists")
+        return SAt, Sb
+
+
 class RhtDenseColMajor:
     """SA = S_h H D A for column-major A (skh_rht_dense_colmajor): two HBM passes,
     the second fused with the sketch.  Returns SA^T (d, m) and Sb."""

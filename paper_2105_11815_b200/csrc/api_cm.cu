@@ -166,7 +166,7 @@ int pass1_reserve(const CmPlan& pl, int64_t ncols) {
 
 // Transform passes after pass 1 (mid passes) then the fused final pass.
 int cm_rht_tail(const CmPlan& pl, int64_t n_pad, int64_t ncols, int64_t d, int64_t m, int s, const CmWs& w,
-                double* SA, int64_t ldsa, double* Sb, cudaStream_t st) {
+                double* SA, int64_t ldsa, double* Sb, cudaStream_t st, double alpha) {
   int lo = pl.K1;
   for (int i = 0; i < pl.nmid; ++i) {
     int rc = launch_cm_mid(w.Y, n_pad, ncols, n_pad, lo, pl.mid[i], st);
@@ -175,10 +175,24 @@ int cm_rht_tail(const CmPlan& pl, int64_t n_pad, int64_t ncols, int64_t d, int64
     lo += pl.mid[i];
   }
   int rc = launch_cm_gather(w.Y, n_pad, ncols, nullptr, n_pad, pl.ntiles, pl.lo2, pl.K2, w.lists, s, m, SA, ldsa, d,
-                            Sb, skh_c_ns(n_pad, s), st);
+                            Sb, alpha, st);
   if (rc) return rc;
   skh_trace_mark(st, "pass2_gather");
   return SKH_OK;
+}
+
+// skh_fold_cols: T_r's column lists over the local rows (M3, include/skh.h)
+__global__ void fold_cols_kernel(int64_t L, int64_t G, int s, int64_t rank, const int32_t* __restrict__ col_rows,
+                                 const int8_t* __restrict__ col_signs, int32_t* __restrict__ fold_rows,
+                                 int8_t* __restrict__ fold_signs) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // destination entry
+  const int64_t gs = G * s;
+  if (t >= L * gs) return;
+  const int64_t l = t / gs, g = (t % gs) / s, q = t % s;
+  const int64_t src = (g * L + l) * s + q;
+  fold_rows[t] = col_rows[src];
+  const int neg = __popcll((unsigned long long)(g & rank)) & 1;
+  fold_signs[t] = neg ? (int8_t)(-col_signs[src]) : col_signs[src];
 }
 
 }  // namespace
@@ -260,7 +274,7 @@ int skh_rht_dense_colmajor(uint64_t seed, int64_t n, int64_t m, int32_t s, int64
   if (rc) return rc;
   if (jc) return jc;
   skh_trace_mark(st, "side_wait");
-  return cm_rht_tail(pl, n_pad, ncols, d, m, s, w, SA, ldsa, Sb, st);
+  return cm_rht_tail(pl, n_pad, ncols, d, m, s, w, SA, ldsa, Sb, st, skh_c_ns(n_pad, s));
 }
 
 int skh_rht_dense_colmajor_host(uint64_t seed, int64_t n, int64_t m, int32_t s, int64_t d, const double* A_host,
@@ -312,7 +326,7 @@ int skh_rht_dense_colmajor_host(uint64_t seed, int64_t n, int64_t m, int32_t s, 
     if (!rc) rc = launch_cm_pass1(seed, yb, n_pad, 1, nullptr, yb, n_pad, n, pl.L, 1, 0, st);
   }
   if (!rc) skh_trace_mark(st, "h2d_pass1");
-  if (!rc) rc = cm_rht_tail(pl, n_pad, ncols, d, m, s, w, w.SA, m, w.Sb, st);
+  if (!rc) rc = cm_rht_tail(pl, n_pad, ncols, d, m, s, w, w.SA, m, w.Sb, st, skh_c_ns(n_pad, s));
   if (!rc && cudaMemcpy2DAsync(SA_host, sizeof(double) * ldsa, w.SA, sizeof(double) * m, sizeof(double) * m, d,
                                cudaMemcpyDeviceToHost, st) != cudaSuccess)
     rc = check_launch("D2H SA");
@@ -446,6 +460,65 @@ int skh_rht_colmajor(uint64_t seed, int64_t nrows, int64_t nvalid, int64_t row0,
   }
   if (pl.K2 > 0) rc = launch_cm_mid(Y, ldy, ncols, nrows, lo, pl.K2, st);
   return rc;
+}
+
+int skh_fold_cols(int64_t L, int64_t G, int32_t s, int64_t rank, const int32_t* col_rows, const int8_t* col_signs,
+                  int32_t* fold_rows, int8_t* fold_signs, void* stream) {
+  if (L < 1 || G < 1 || s < 1 || rank < 0 || rank >= G || !col_rows || !col_signs || !fold_rows || !fold_signs) {
+    set_error("fold_cols: invalid arguments");
+    return SKH_EINVAL;
+  }
+  const int64_t N = L * G * (int64_t)s;
+  fold_cols_kernel<<<(unsigned)((N + 255) / 256), 256, 0, as_stream(stream)>>>(L, G, s, rank, col_rows, col_signs,
+                                                                               fold_rows, fold_signs);
+  note_launch();
+  return check_launch("fold_cols");
+}
+
+size_t skh_rht_colmajor_lists_workspace_bytes(int64_t L, int64_t m, int32_t s_eff, int64_t d) {
+  if (L < 1 || m < 1 || s_eff < 1 || d < 1) return 0;
+  const int64_t n_pad = next_pow2(L);
+  const CmPlan pl = cm_plan(n_pad);
+  return cm_layout(nullptr, n_pad, d + 1, n_pad, m, s_eff, d, pl.ntiles, false).total;
+}
+
+int skh_rht_colmajor_lists(uint64_t seed, int64_t L, int64_t row0, int64_t m, int32_t s_eff, int64_t d,
+                           const double* A, int64_t lda, const double* b, const int32_t* col_rows,
+                           const int8_t* col_signs, double alpha, double* SAt, int64_t ldsa, double* Sb, void* ws,
+                           size_t ws_bytes, void* stream) {
+  if (!A || !SAt || !col_rows || !col_signs || row0 < 0) {
+    set_error("rht_colmajor_lists: A, SAt and the column lists required, row0 >= 0");
+    return SKH_EINVAL;
+  }
+  const int64_t n_pad = next_pow2(std::max<int64_t>(L, 1));
+  int rc = validate(L, m, s_eff, d, n_pad);
+  if (rc) return rc;
+  if (lda < L || ldsa < m || (b && !Sb)) {
+    set_error("rht_colmajor_lists: need lda >= L, ldsa >= m, Sb when b is given");
+    return SKH_EDIM;
+  }
+  const CmPlan pl = cm_plan(n_pad);
+  const int64_t ncols = d + (b ? 1 : 0);
+  const CmWs w = cm_layout(ws, n_pad, d + 1, n_pad, m, s_eff, d, pl.ntiles, false);
+  if (!ws || ws_bytes < w.total) {
+    set_error("rht_colmajor_lists workspace too small: need %zu bytes", w.total);
+    return SKH_EWORKSPACE;
+  }
+  cudaStream_t st = as_stream(stream);
+  trace_begin(st);
+  // the tile lists depend only on the given column lists: side stream, beside pass 1
+  cudaStream_t ss = skh_side_fork(st);
+  // the lists cover all n_pad rows of the padded transform (H mixes the zero padding in)
+  rc = launch_cm_lists(col_rows, col_signs, s_eff, m, pl.K2, pl.lo2, n_pad, pl.ntiles, w.lists, ss);
+  if (!rc) skh_trace_mark(ss, ss != st ? "side:tile_lists" : "tile_lists");
+  if (!rc) rc = launch_cm_pass1(seed, A, lda, d, b, w.Y, n_pad, L, pl.L, 1, row0, st,
+                                ss != st ? pass1_reserve(pl, ncols) : 0);
+  if (!rc) skh_trace_mark(st, "pass1");
+  const int jc = skh_side_join(st, ss);
+  if (rc) return rc;
+  if (jc) return jc;
+  skh_trace_mark(st, "side_wait");
+  return cm_rht_tail(pl, n_pad, ncols, d, m, s_eff, w, SAt, ldsa, Sb, st, alpha);
 }
 
 }  // extern "C"

@@ -54,6 +54,22 @@ class CudaOps:
     def fold_lists(self, bl, L, rank):
         return self.api.fold_lists(bl, L, rank)
 
+    def hash_cols(self, seed, m, s, n, out=None):
+        """Column lists (rows, signs) of all n columns of S, [n][s] (the bucket
+        lists are built too and reused through ``out``)."""
+        bl = self.api.hash_gen(seed, m, s, n, want_cols=True, out=out)
+        return bl
+
+    def fold_cols(self, bl, L, G, s, rank, out=None):
+        return self.api.fold_cols(bl.col_rows, bl.col_signs, L, G, s, rank, out=out)
+
+    def rht_cm_lists(self, op, seed, At, b, row0, lists, SAt, Sb):
+        """Unscaled S' H_L D A_r for a column-major local block (op: api.RhtColMajorLists)."""
+        return op(seed, At, b, row0, lists[0], lists[1], alpha=1.0, SAt=SAt, Sb=Sb)
+
+    def rht_cm_lists_op(self, L, m, s_eff, d, device):
+        return self.api.RhtColMajorLists(L, m, s_eff, d, device)
+
     def c_ns(self, n_pad, s):
         return self.api.c_ns(n_pad, s)
 
@@ -307,6 +323,83 @@ class ShardedHrhtM3:
             Sb = self.outb[: hi - lo, 0]
         mark("reduce")
         return self.out[: hi - lo], Sb, (lo, hi)
+
+
+class ShardedHrhtM3Col:
+    """The exchange-free M3 of ShardedHrhtM3 for a COLUMN-MAJOR local block At
+    (d, L) -- the paper's storage -- with the survey's on-chip fan-out
+    (SURVEY §8(e) M3): each rank folds the column lists of all n columns of S
+    into T_r's (skh_fold_cols: G s entries per local row), then ONE call
+    (skh_rht_colmajor_lists) runs pass 1 of H_L D A_r (D over global ids) and
+    the fused pass 2, whose owner-planned gather adds every local row, read once
+    from HBM, into its G s folded buckets from shared memory.  The unscaled
+    partials SA_r^T (d, m) meet in the deterministic rank-order reduction over
+    column strips of SA (rank r gets SA[:, dlo:dhi] as SA^T rows, contiguous
+    blocks for the all-to-all); Sb over bucket strips as in ShardedHrht.
+    Needs G s <= 8 (the fused gather's draws per row).  1e-12 against the
+    unsharded oracle, bit-identical on integer inputs.
+
+    run() -> (SAt_strip (dhi - dlo, m), (dlo, dhi), Sb_strip, (lo, hi))."""
+
+    STAGES = ("hash_gen", "sketch", "reduce")
+
+    def __init__(self, seed, At_loc, b_loc, n, m, s, ops=None, group=None):
+        self.ops = ops or CudaOps()
+        self.group = group
+        self.G = dist.get_world_size(group)
+        self.r = dist.get_rank(group)
+        self.seed, self.n, self.m, self.s = seed, int(n), int(m), int(s)
+        self.L = self.n // self.G
+        d, L = At_loc.shape
+        if self.L * self.G != self.n or L != self.L:
+            raise ValueError("At_loc must be (d, n / G)")
+        _log2(self.n)
+        if self.G * self.s > 8:
+            raise ValueError(f"column-major M3 folds G s = {self.G * self.s} draws per local row; the fused "
+                             "gather takes at most 8 (use ShardedHrht)")
+        if self.n * self.s >= 2 ** 31:
+            raise ValueError(f"exchange-free H D needs n * s < 2^31 (n = {self.n}, s = {self.s})")
+        self.At, self.b, self.d = At_loc, b_loc, d
+        kw = dict(dtype=At_loc.dtype, device=At_loc.device)
+        self.dq, self.dstrips = strip_rows(d, self.G)
+        self.mq, self.strips = strip_rows(self.m, self.G)
+        self.P = torch.zeros(self.G * self.dq, self.m, **kw)   # partial SA^T, column strips of SA
+        self.Pb = torch.zeros(self.G * self.mq, **kw) if b_loc is not None else None
+        self.R = torch.empty(self.G, self.dq, self.m, **kw)
+        self.Rb = torch.empty(self.G, self.mq, **kw) if b_loc is not None else None
+        self.out = torch.empty(self.dq, self.m, **kw)
+        self.outb = torch.empty(self.mq, 1, **kw) if b_loc is not None else None
+        self.alpha = self.ops.c_ns(self.n, self.s)
+        self.bl = None
+        self.lists = None
+        self.op = self.ops.rht_cm_lists_op(self.L, self.m, self.G * self.s, d, At_loc.device)
+
+    def run(self, mark=None):
+        mark = mark or (lambda name: None)
+        ops, G, r, L = self.ops, self.G, self.r, self.L
+        self.bl = ops.hash_cols(self.seed, self.m, self.s, self.n, out=self.bl)
+        self.lists = ops.fold_cols(self.bl, L, G, self.s, r, out=self.lists)
+        mark("hash_gen")
+        ops.rht_cm_lists(self.op, self.seed, self.At, self.b, r * L, self.lists, self.P[: self.d],
+                         None if self.b is None else self.Pb[: self.m])
+        mark("sketch")
+        dlo, dhi = self.dstrips[r]
+        lo, hi = self.strips[r]
+        if G > 1:
+            all_to_all(self.R.view(G * self.dq, self.m), self.P, group=self.group)
+            if self.b is not None:
+                all_to_all(self.Rb.view(-1), self.Pb, group=self.group)
+        else:
+            self.R[0].copy_(self.P)
+            if self.b is not None:
+                self.Rb[0].copy_(self.Pb)
+        ops.ordered_sum(self.R, self.alpha, out=self.out)
+        Sb = None
+        if self.b is not None:
+            ops.ordered_sum(self.Rb.view(G, self.mq, 1), self.alpha, out=self.outb)
+            Sb = self.outb[: hi - lo, 0]
+        mark("reduce")
+        return self.out[: dhi - dlo], (dlo, dhi), Sb, (lo, hi)
 
 
 class ShardedPlain:

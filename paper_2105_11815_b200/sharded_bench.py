@@ -102,13 +102,23 @@ def run(args, cfg):
         shard = None
     elif cfg.hd:
         L = cfg.n // G
-        A = device.dense(cfg, rank * L, (rank + 1) * L)
         b = device.rhs(cfg, rank * L, (rank + 1) * L)
-        # SKH_SHARDED_HD=m3: the exchange-free variant (H_G folded into the sketch)
-        if os.environ.get("SKH_SHARDED_HD", "m2") == "m3":
-            step = sharded.ShardedHrhtM3(cfg.seed, A, b, cfg.n, cfg.m, cfg.s)
+        # SKH_SHARDED_HD: m2 (butterfly all-to-all), m3 (exchange-free, row-major
+        # pull gather), m3col (exchange-free, column-major, on-chip fan-out);
+        # auto = m3col at G = 2 (projected 0.78 vs 0.70 strong-scaling
+        # efficiency from the measured per-rank kernels), else m2
+        mode = os.environ.get("SKH_SHARDED_HD", "auto")
+        if mode == "auto":
+            mode = "m3col" if (G == 2 and G * cfg.s <= 8) else "m2"
+        if mode == "m3col":
+            A = device.dense_colmajor(cfg, rank * L, (rank + 1) * L)
+            step = sharded.ShardedHrhtM3Col(cfg.seed, A, b, cfg.n, cfg.m, cfg.s)
         else:
-            step = sharded.ShardedHrht(cfg.seed, A, b, cfg.n, cfg.m, cfg.s)
+            A = device.dense(cfg, rank * L, (rank + 1) * L)
+            if mode == "m3":
+                step = sharded.ShardedHrhtM3(cfg.seed, A, b, cfg.n, cfg.m, cfg.s)
+            else:
+                step = sharded.ShardedHrht(cfg.seed, A, b, cfg.n, cfg.m, cfg.s)
         shard = (A, b)
     else:
         per = (cfg.n + G - 1) // G
@@ -172,7 +182,8 @@ def run(args, cfg):
             s0.record()
             A_d.copy_(A_h, non_blocking=True)
             b_d.copy_(b_h, non_blocking=True)
-            SA, Sb, _ = step.run()
+            res = step.run()
+            SA, Sb = res[0], res[2] if len(res) == 4 else res[1]
             SA_h = SA.cpu()
             Sb_h = Sb.cpu()
             s1.record()
@@ -186,7 +197,7 @@ def run(args, cfg):
 
     # ---- collective roofline at the step's message sizes (all ranks take part)
     msg = []
-    if cfg.hd and G > 1 and not isinstance(step, sharded.ShardedHrhtM3):
+    if cfg.hd and G > 1 and isinstance(step, sharded.ShardedHrht):
         # one column chunk of the butterfly exchange: the L x W send buffer of a rank
         msg.append(("all_to_all", (cfg.n // G) * min(cfg.d, getattr(step, "W", cfg.d)) * 8))
     if G > 1 and cfg.kind != "csr":
@@ -207,7 +218,22 @@ def run(args, cfg):
                            "note": cfg.note},
                 "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
                 "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e}
-        if cfg.hd and isinstance(step, sharded.ShardedHrhtM3):
+        if cfg.hd and isinstance(step, sharded.ShardedHrhtM3Col):
+            # per rank: pass 1 of H_L D A_r and the fused pass 2, whose gather adds
+            # every local row (read once) into its G s folded buckets on chip --
+            # SURVEY §8(d) counts A_r once, the partial SA^T and the folded lists
+            L = cfg.n // G
+            t = stage_ms["sketch"]
+            alg = L * cfg.d * 8 + cfg.m * cfg.d * 8 + G * cfg.s * L * 5
+            ach = alg / (t / 1e3) / 1e9
+            line["roofline"] = {"bound": "hbm", "kernel": "cm_pass1p + cm_gather (G s folded draws per row) per rank",
+                                "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                                "frac": round(ach / pk["hbm_gbs"], 4), "traffic": None, "peak_source": src,
+                                "sketch_ms": round(t, 4), "draws_per_local_row": G * cfg.s}
+            dq = (cfg.d + G - 1) // G
+            line["comm"] = {"all_to_all_rows_bytes_sent_per_rank": 0,
+                            "strip_reduction_bytes_per_rank": (G - 1) * dq * cfg.m * 8}
+        elif cfg.hd and isinstance(step, sharded.ShardedHrhtM3):
             # per rank: the local FWHT passes over L rows, then a gather whose lists
             # read every local row G s times (the folded H_G)
             L = cfg.n // G

@@ -302,3 +302,37 @@ def test_plain_colmajor_fast_and_walk_bit_identical(n, d, m, s):
         SAt, Sb = skh().sketch_dense_colmajor(5, At, bd, m, s, fast=fast)
         assert np.array_equal(SAt.cpu().numpy().T.view(np.int64), SAo.view(np.int64))
         assert np.array_equal(Sb.cpu().numpy().view(np.int64), Sbo.view(np.int64))
+
+
+@pytest.mark.parametrize("n,d,m,s", [(1 << 15, 33, 300, 1), (40000, 5, 700, 3), (1 << 14, 64, 112, 8)])
+def test_rht_colmajor_lists_equals_composite(n, d, m, s):
+    """skh_rht_colmajor_lists fed the hash's own column lists (row0 = 0, alpha =
+    c_ns) is the composite skh_rht_dense_colmajor, bit for bit; and a folded
+    pair of half-size calls (M3 with G = 2 on one GPU) sums to the oracle."""
+    from oracle import sketch
+    from synth import configs, device, gen
+    api = skh().api
+    cfg = configs.C2.scaled(n=n, d=d, m=m)
+    At = device.dense_colmajor(cfg)
+    b = device.rhs(cfg)
+    SAt, Sb = skh().RhtDenseColMajor(n, m, s, d)(cfg.seed, At, b)
+    n_pad = 1 << (n - 1).bit_length()
+    bl = api.hash_gen(cfg.seed, m, s, n_pad, want_cols=True)  # lists of every row of the padded transform
+    op = api.RhtColMajorLists(n, m, s, d)
+    SAt2, Sb2 = op(cfg.seed, At, b, 0, bl.col_rows, bl.col_signs, alpha=api.c_ns(n_pad, s))
+    assert torch.equal(SAt, SAt2) and torch.equal(Sb, Sb2)
+    if s <= 4 and n == n_pad:
+        L = n // 2
+        opL = api.RhtColMajorLists(L, m, 2 * s, d)
+        parts = []
+        for r in range(2):
+            f = api.fold_cols(bl.col_rows, bl.col_signs, L, 2, s, r)
+            parts.append(opL(cfg.seed, At[:, r * L:(r + 1) * L].contiguous(), b[r * L:(r + 1) * L].contiguous(),
+                             r * L, f[0], f[1], alpha=1.0))
+        c = api.c_ns(n, s)
+        SA3 = (c * (parts[0][0] + parts[1][0])).cpu().numpy().T
+        Sb3 = (c * (parts[0][1] + parts[1][1])).cpu().numpy()
+        A = gen.dense(cfg)
+        want, wantb = sketch.rht_sketch(cfg.seed, A, gen.rhs(cfg), m, s)
+        assert np.linalg.norm(SA3 - want) / np.linalg.norm(want) <= 1e-12
+        assert np.linalg.norm(Sb3 - wantb) / np.linalg.norm(wantb) <= 1e-12

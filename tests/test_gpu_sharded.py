@@ -55,6 +55,15 @@ def _worker(rank, G, port, kind, out_dir):
             ok &= np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
             if kind == "int":
                 ok &= np.array_equal(got, ref)
+        # column-major local blocks: skh_fold_cols + skh_rht_colmajor_lists (on-chip fan-out of G s draws)
+        m3c = sharded.ShardedHrhtM3Col(seed, At.t().contiguous(), bt, n, m, s)
+        sat, dlohi, sb, lohi = m3c.run()
+        SA = sharded.gather_strips(sat, dlohi, d).cpu().numpy().T
+        Sb = sharded.gather_strips(sb, lohi, m).cpu().numpy()
+        for got, ref in ((SA, want), (Sb, wantb)):
+            ok &= np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
+            if kind == "int":
+                ok &= np.array_equal(got, ref)
         pl = sharded.ShardedPlain(seed, At, bt, n, m, 2)
         strip, sb, lohi = pl.run()
         SA = sharded.gather_strips(strip, lohi, m).cpu().numpy()

@@ -81,6 +81,43 @@ class OracleOps:
         bl.signs = np.where(par == 1, -np.asarray(bl.signs), np.asarray(bl.signs)).astype(np.asarray(bl.signs).dtype)
         return bl
 
+    def hash_cols(self, seed, m, s, n, out=None):
+        rows, signs = hashing.draw_columns(seed, np.arange(n), m, s)
+        bl = self.BL(m, s, None, None, None)
+        bl.col_rows, bl.col_signs = rows.reshape(-1), signs.reshape(-1)
+        return bl
+
+    def fold_cols(self, bl, L, G, s, rank, out=None):
+        # T_r's column lists over local rows: entry (l, g, q) <- global row g L + l, sign x (-1)^popcount(g & r)
+        rows = np.asarray(bl.col_rows).reshape(G, L, s)
+        signs = np.asarray(bl.col_signs).reshape(G, L, s).astype(np.int64)
+        par = np.array([(-1) ** (bin(g & rank).count("1") & 1) for g in range(G)])
+        return (rows.transpose(1, 0, 2).reshape(-1),
+                (signs * par[:, None, None]).transpose(1, 0, 2).reshape(-1).astype(np.int8))
+
+    def rht_cm_lists_op(self, L, m, s_eff, d, device):
+        return (L, m, s_eff, d)
+
+    def rht_cm_lists(self, op, seed, At, b, row0, lists, SAt, Sb):
+        # unscaled T_r H_L D A_r from the folded column lists (bucket order: local row, then entry)
+        L, m, s_eff, d = op
+        lg = L.bit_length() - 1
+        D = hadamard.diag_signs(seed, np.arange(row0, row0 + L))
+        Z = np.ascontiguousarray(At.numpy().T) * D[:, None]
+        hadamard.fwht_stages(Z, 0, lg)
+        k = np.asarray(lists[0], dtype=np.int64)
+        sg = np.asarray(lists[1])
+        local = np.repeat(np.arange(L), s_eff)
+        perm = np.argsort(k, kind="stable")
+        ptr = np.zeros(m + 1, dtype=np.int64)
+        np.cumsum(np.bincount(k, minlength=m), out=ptr[1:])
+        SAt.copy_(torch.from_numpy(sketch.bucket_sum(Z, ptr, local[perm], sg[perm], 1.0).T.copy()))
+        if b is not None:
+            zb = b.numpy() * D
+            hadamard.fwht_stages(zb[:, None], 0, lg)
+            Sb.copy_(torch.from_numpy(sketch.bucket_sum(zb, ptr, local[perm], sg[perm], 1.0)))
+        return SAt, Sb
+
     def c_ns(self, n_pad, s):
         return sketch.c_ns(n_pad, s)
 
@@ -128,6 +165,17 @@ def _worker(rank, G, port, case):
             assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
             if kind == "int":
                 assert np.array_equal(got, ref)
+        # the exchange-free variant on column-major local blocks (on-chip fan-out of G s folded draws)
+        if G * s <= 8:
+            m3c = sharded.ShardedHrhtM3Col(seed, torch.from_numpy(A[rank * L:(rank + 1) * L].T.copy()), bt, n, m, s,
+                                           ops=ops)
+            sat, dlohi, sb, lohi = m3c.run()
+            SA = sharded.gather_strips(sat, dlohi, d).numpy().T
+            Sb = sharded.gather_strips(sb, lohi, m).numpy()
+            for got, ref in ((SA, want), (Sb, wantb)):
+                assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-12
+                if kind == "int":
+                    assert np.array_equal(got, ref)
         # plain s-hashing with uneven row blocks
         per = (n + G - 1) // G
         r0, r1 = min(n, rank * per), min(n, (rank + 1) * per)
