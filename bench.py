@@ -433,7 +433,54 @@ def gpu_arm_single(args, cfg):
         torch.cuda.empty_cache()
     if cpu_line is not None:
         line["cpu_baseline"] = cpu_line
+    if args.sketch == "hashing" and not args.no_all_workloads:
+        line["workloads"] = other_workloads_measure(args, cfg, torch, pk, src)
     print(json.dumps(line), flush=True)
+
+
+def other_workloads_measure(args, main_cfg, torch, pk, src):
+    """The other BASELINE configs in the same run (so the driver's clock covers
+    them too): each in its default layout, W warm-up + min(K, 10) timed steps,
+    the step's SURVEY §8(d) alg_frac and a whole-matrix Freivalds check of its
+    SA (the oracle leg).  Reported beside the headline, not instead of it."""
+    from synth import configs
+    out = {}
+    for name in ("C1", "C2", "C3", "C3HD", "C4", "C5"):
+        cfg = configs.ALL[name]
+        if name == main_cfg.name:
+            continue
+        layout = default_layout(cfg)
+        step, inputs = build_step(cfg, torch, layout)
+        torch.cuda.synchronize()
+        for _ in range(max(args.warmup, 0)):
+            step.run()
+        steps = max(1, min(args.steps, 10))
+        timers = [step.new_timer() for _ in range(steps)]
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for k in range(steps):
+            step.run(timers[k])
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        per = [t.durations_ms() for t in timers]
+        stage_ms = {k: sum(p[k] for p in per) / len(per) for k in per[0]}
+        rl = roofline(cfg, step, stage_ms, ms, pk["hbm_gbs"], src, layout)
+        rec = {"value": round(cfg.a_bytes / (ms / 1e3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
+               "steps": steps, "layout": "column-major" if layout == "col" else "row-major",
+               "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+               "alg_frac": rl["step"]["alg_frac"], "kernel": rl["kernel"], "kernel_frac": rl["frac"]}
+        if not args.no_cpu_baseline:
+            SA = step.run()[0]
+            torch.cuda.synchronize()
+            fv = freivalds_check(cfg, SA, inputs, layout)
+            rec["freivalds_ok"], rec["freivalds_worst_rel"] = fv["ok"], fv["worst_rel"]
+            del SA
+        out[name] = rec
+        del step, inputs
+        torch.cuda.empty_cache()
+    return out
 
 
 def alt_layout_measure(args, cfg, torch, pk, src, layout):
@@ -484,6 +531,8 @@ def main():
     ap.add_argument("--no-alt-layout", action="store_true",
                     help="skip the column-major measurement reported beside a row-major H D workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-all-workloads", action="store_true",
+                    help="skip the other BASELINE configs reported beside the headline (line key 'workloads')")
     args = ap.parse_args()
     from synth import configs
     cfg = configs.ALL[args.workload]

@@ -7,7 +7,7 @@ mkdir -p "$out"
 for w in ${@:-C5 C2 C3HD C3 C4 C1}; do
   for lay in auto row; do
     [ "$lay" = row ] && [ "$w" != C5 ] && continue
-    cmd="python bench.py --workload $w --layout $lay --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-alt-layout"
+    cmd="python bench.py --workload $w --layout $lay --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-alt-layout --no-all-workloads"
     $cmd > "$out/plain_${w}_${lay}.log" 2>&1 && \
     ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
         --csv --log-file "$out/launches_${w}_${lay}.csv" $cmd > "$out/ncu_${w}_${lay}.log" 2>&1
