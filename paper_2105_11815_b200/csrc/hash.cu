@@ -518,7 +518,11 @@ int launch_hash_v(uint64_t seed, int64_t m, int s, int64_t nrows, int64_t row0, 
     const char* e = getenv("SKH_HASH_RADIX");
     return e && atoi(e) != 0;
   }();
-  if (N > 0 && !force_radix && use_segmented(N, m)) {
+  static const bool force_seg = [] {  // measurement switch: the segmented path at any bucket size
+    const char* e = getenv("SKH_HASH_SEG");
+    return e && atoi(e) != 0;
+  }();
+  if (N > 0 && !force_radix && (use_segmented(N, m) || (force_seg && m >= 64 && m <= (1 << 20)))) {
     cudaMemsetAsync(w.status, 0, sizeof(int32_t), st);
     return launch_hash_seg(seed, m, s, nrows, row0, blk, stride, col_rows, col_signs, bucket_ptr, bucket_rows,
                            bucket_signs, w, counts, variant, st);
