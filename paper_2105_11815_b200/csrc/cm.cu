@@ -241,6 +241,111 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// mbarrier helpers (CTA scope)
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void nbar(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
+
+// Persistent pass 1 with two teams of 8 warps per CTA (512 threads, one CTA
+// per SM): team k takes the CTA's chunks i = k, k + 2, ...; chunk i lives in
+// ring slot i % 3.  At the start of chunk i a team issues the cp.async copies
+// of chunk i + 1 -- the OTHER team's next chunk -- into slot (i + 1) % 3, which
+// held chunk i - 2 (its own, finished); each issuing thread's copies arrive on
+// the slot's mbarrier (cp.async.mbarrier.arrive.noinc, 256 arrivals per
+// phase), on which the other team waits.  While one team runs its butterflies
+// the other's shared-memory phases and loads are in flight: twice the warps of
+// cm_pass1p_kernel per SM.  Same stages, same order: bit-identical to it.
+template <bool DIAG>
+__global__ void __launch_bounds__(512, 1)
+    cm_pass1t_kernel(const double* __restrict__ X, int64_t ldx, int64_t ncolX, const double* __restrict__ xb,
+                     double* __restrict__ Y, int64_t ldy, int64_t nchunks, int64_t total, uint64_t dkey,
+                     int64_t row0) {
+  extern __shared__ __align__(16) double2 smp[];  // [3][4096], swizzled
+  __shared__ __align__(8) uint64_t full[3];
+  const int tid = threadIdx.x, team = tid >> 8, t = tid & 255;
+  if (tid < 3) mbar_init(&full[tid], 256);
+  __syncthreads();
+  auto issue = [&](int64_t item, int slot) {  // 256 threads of one team
+    const int64_t c = item / nchunks;
+    const double2* src = reinterpret_cast<const double2*>(col_in(X, ldx, ncolX, xb, c) + ((item % nchunks) << kP1Bits));
+    double2* dsm = smp + slot * 4096;
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {
+      const int q = t + 256 * v;
+      const unsigned d = (unsigned)__cvta_generic_to_shared(dsm + swz(q));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + q));
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&full[slot]))
+                 : "memory");
+  };
+  const int64_t G = gridDim.x;
+  if (team == 0 && (int64_t)blockIdx.x < total) issue(blockIdx.x, 0);  // chunk 0
+  const int bar = 1 + team;
+  for (int64_t i = team;; i += 2) {
+    const int64_t item = (int64_t)blockIdx.x + i * G;
+    if (item >= total) break;
+    const int slot = (int)(i % 3);
+    nbar(bar);  // this team's reads of chunk i - 2 (slot (i + 1) % 3) are done
+    if (item + G < total) issue(item + G, (int)((i + 1) % 3));
+    mbar_wait(&full[slot], (unsigned)((i / 3) & 1));
+    double2* sm = smp + slot * 4096;
+    const int64_t c = item / nchunks;
+    const int64_t base = (item % nchunks) << kP1Bits;
+    double2 x[16];
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = sm[swz(v | (t << 4))];
+    if (DIAG) {
+      const int64_t g0 = row0 + base + 32 * t;
+      const int sh = (int)(g0 & 63);
+      uint64_t win = stream_u(dkey, (uint64_t)(g0 >> 6)) >> sh;
+      if (sh > 32) win |= stream_u(dkey, (uint64_t)((g0 >> 6) + 1)) << (64 - sh);
+      const uint32_t neg = (uint32_t)win;
+#pragma unroll
+      for (int v = 0; v < 16; ++v) {
+        if ((neg >> (2 * v)) & 1u) x[v].x = -x[v].x;
+        if ((neg >> (2 * v + 1)) & 1u) x[v].y = -x[v].y;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {  // element bit 0
+      const double a = x[v].x, b = x[v].y;
+      x[v] = make_double2(a + b, a - b);
+    }
+    stages16(x);  // element bits 1-4
+    nbar(bar);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) sm[swz(v | (t << 4))] = x[v];
+    nbar(bar);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = sm[swz((t & 15) | (v << 4) | ((t >> 4) << 8))];
+    stages16(x);  // element bits 5-8
+    nbar(bar);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) sm[swz((t & 15) | (v << 4) | ((t >> 4) << 8))] = x[v];
+    nbar(bar);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = sm[swz(t | (v << 8))];
+    stages16(x);  // element bits 9-12
+    double2* dst = reinterpret_cast<double2*>(Y + c * ldy + base);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) dst[t | (v << 8)] = x[v];
+  }
+}
+
 // Columns of at most 2^12 rows: the whole column in shared memory, stages one
 // at a time (small problems only).
 template <bool DIAG>
@@ -948,6 +1053,23 @@ int launch_cm_pass1(uint64_t seed, const double* X, int64_t ldx, int64_t ncolX, 
   const bool vec = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(xb) |
                      reinterpret_cast<uintptr_t>(Y)) % 16 == 0) &&
                    (ldx % 2 == 0 || ncolX <= 1) && (ldy % 2 == 0);
+  static const bool teams = [] {  // SKH_P1_TEAMS=0: the one-team persistent kernel
+    const char* e = getenv("SKH_P1_TEAMS");
+    return !(e && e[0] == '0');
+  }();
+  if (teams && vec && nvalid >= ((int64_t)1 << L)) {  // every chunk full: two teams per CTA
+    const size_t smem = (size_t)kP1Ring * 65536;
+    const int64_t total = grid;
+    const int64_t g = std::min<int64_t>(total, (int64_t)std::max(1, num_sms() - std::max(0, reserve_sms)));
+    int rc = apply_diag ? set_smem(cm_pass1t_kernel<true>, smem) : set_smem(cm_pass1t_kernel<false>, smem);
+    if (rc) return rc;
+    if (apply_diag)
+      cm_pass1t_kernel<true><<<(unsigned)g, 512, smem, st>>>(X, ldx, ncolX, xb, Y, ldy, nchunks, total, dkey, row0);
+    else
+      cm_pass1t_kernel<false><<<(unsigned)g, 512, smem, st>>>(X, ldx, ncolX, xb, Y, ldy, nchunks, total, dkey, row0);
+    note_launch();
+    return check_launch("cm_pass1t");
+  }
   if (vec && nvalid >= ((int64_t)1 << L)) {  // every chunk full: the persistent double-buffered kernel
     const size_t smem = (size_t)kP1Ring * 65536;
     const int64_t total = grid;
