@@ -278,7 +278,21 @@ def test_determinism_stress_shared_memory_paths():
     # the HR-DHT passes (shared-memory FFT rounds)
     A2 = device.dense(configs.C2.scaled(n=1 << 14, d=40, m=100))
     runs8 = [skh().hrdht_dense(3, A2, None, 100, 2) for _ in range(5)]
-    for rr in (runs, runs2, runs3, runs4, runs5, runs6, runs7, runs8):
+    # the 16-lane row gather (s > 1, 64-column slices) and the M3 rank step with
+    # folded lists (two-team pass 1 + fused pass 2 with s_eff = 2 draws per row)
+    c3 = configs.C3.scaled(n=20000, d=256, m=300)
+    A3 = device.dense(c3)
+    bl3 = skh().hash_gen(c3.seed, c3.m, c3.s, c3.n)
+    runs9 = [skh().sketch_dense(bl3, A3, device.rhs(c3)) for _ in range(5)]
+    api = skh().api
+    cm3 = configs.C5.scaled(n=1 << 18, d=3, m=700)
+    L = cm3.n // 2
+    Atm = device.dense_colmajor(cm3, L, cm3.n)
+    blc = api.hash_gen(cm3.seed, cm3.m, 1, cm3.n, want_cols=True)
+    f = api.fold_cols(blc.col_rows, blc.col_signs, L, 2, 1, 1)
+    opm = api.RhtColMajorLists(L, cm3.m, 2, cm3.d)
+    runs10 = [tuple(t.clone() for t in opm(cm3.seed, Atm, None, L, f[0], f[1])[:1]) + (None,) for _ in range(5)]
+    for rr in (runs, runs2, runs3, runs4, runs5, runs6, runs7, runs8, runs9, runs10):
         for SA, Sb in rr[1:]:
             assert torch.equal(SA, rr[0][0])
             if Sb is not None:
