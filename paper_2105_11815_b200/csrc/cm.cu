@@ -588,8 +588,8 @@ constexpr int kBarProd = 1, kBarCons = 2, kBarFull = 3, kBarEmpty = 3 + kNBuf;
 __host__ __device__ constexpr size_t plan_smem_bytes(int s, int nb) {
   return (size_t)4 * kE * s + sizeof(int) * (size_t)nb_pad(nb) + 16;
 }
-__host__ __device__ constexpr size_t gather_smem_bytes(int nb) {
-  return (size_t)kNBuf * kE * 8 + 8 * (size_t)nb_pad(nb);
+__host__ __device__ constexpr size_t gather_smem_bytes(int nb, int ncol = 1) {
+  return (size_t)ncol * ((size_t)kNBuf * kE * 8 + 8 * (size_t)nb_pad(nb));
 }
 
 // Warp-specialised (one CTA per SM, 512 threads): warps 0-7 produce -- load a
@@ -597,55 +597,68 @@ __host__ __device__ constexpr size_t gather_smem_bytes(int nb) {
 // exchange through the staging buffer when K2 > 4), leave the final values in
 // staging buffer b -- while warps 8-15 consume the other buffer with the owner
 // plan.  FULL[b] / EMPTY[b] named barriers hand the buffers over.
-template <int K2>
+// NCOL = 2 (small m): the CTA carries TWO columns through every tile -- the
+// producers stage both columns' tiles (two halves of buffer b), the consumers
+// decode each plan word once and add it into both sketches (each column's adds
+// in the same order as NCOL = 1: bit-identical results).
+template <int K2, int NCOL>
 __global__ void __launch_bounds__(kNP + kNC, 1) cm_gather_kernel(const PassArgs a) {
   constexpr int NALL = kNP + kNC;
   extern __shared__ __align__(16) unsigned char smraw[];
-  double* buf = reinterpret_cast<double*>(smraw);                             // [kNBuf][kE]
-  double* sa = reinterpret_cast<double*>(smraw + (size_t)kNBuf * kE * 8);    // [nb_pad + 16]
+  double* buf = reinterpret_cast<double*>(smraw);                                   // [kNBuf][NCOL][kE]
+  double* sa = reinterpret_cast<double*>(smraw + (size_t)kNBuf * NCOL * kE * 8);   // [NCOL][nb_pad]
   const int tid = threadIdx.x;
-  const int64_t my_cols = a.ncols > blockIdx.x ? (a.ncols - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t nitems = my_cols * a.ntiles;
-  // items i = (column, tile) in order: this CTA's columns blockIdx.x, + gridDim.x, ...
+  const int nbp = nb_pad(a.nb);
+  // the CTA's column groups g = blockIdx.x, + gridDim.x, ...; group g = columns NCOL g .. NCOL g + NCOL - 1
+  const int64_t ngroups = (a.ncols + NCOL - 1) / NCOL;
+  const int64_t my_groups = ngroups > blockIdx.x ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t nitems = my_groups * a.ntiles;
   if (tid < kNP) {
     const int t = tid;
     double x[16], xn[16];
-    int64_t ncol = blockIdx.x, ntt = 0;  // the item whose loads are in flight
+    int64_t ngrp = blockIdx.x, ntt = 0;  // the (group, tile) of the loads in flight
+    int nh = 0;                          // ... and which column of the group
     uint64_t pbn = 0;
     if (nitems > 0) {
-      load_tile<K2>(a, ncol, ntt, t, xn);
+      load_tile<K2>(a, NCOL * ngrp, ntt, t, xn);
       pbn = __ldg(a.pbank + ntt * kNP + t);
     }
     for (int64_t i = 0; i < nitems; ++i) {
       const int b = (int)(i % kNBuf);
-      const uint64_t pb = pbn;
 #pragma unroll
-      for (int v = 0; v < 16; ++v) x[v] = xn[v];
-      if (++ntt == a.ntiles) {
-        ntt = 0;
-        ncol += gridDim.x;
+      for (int h = 0; h < NCOL; ++h) {
+        const uint64_t pb = pbn;
+#pragma unroll
+        for (int v = 0; v < 16; ++v) x[v] = xn[v];
+        if (++nh == NCOL) {  // advance (group, tile, column)
+          nh = 0;
+          if (++ntt == a.ntiles) {
+            ntt = 0;
+            ngrp += gridDim.x;
+          }
+        }
+        if (i + 1 < nitems || h + 1 < NCOL) {
+          load_tile<K2>(a, NCOL * ngrp + nh, ntt, t, xn);
+          pbn = __ldg(a.pbank + ntt * kNP + t);
+        }
+        phase0_stages<K2>(x);
+        if (h == 0 && i >= kNBuf) nbar_sync(kBarEmpty + b, NALL);  // the consumers are done with buffer b
+        double* ex = buf + ((size_t)b * NCOL + h) * kE;
+        if constexpr (K2 > 4) {
+#pragma unroll
+          for (int v = 0; v < 16; ++v) ex[Geo<K2>::p0(t, v)] = x[v];
+          nbar_sync(kBarProd, kNP);
+#pragma unroll
+          for (int v = 0; v < 16; ++v) x[v] = ex[Geo<K2>::p1(t, v)];
+          phase1_stages<K2>(x);
+          nbar_sync(kBarProd, kNP);  // exchange reads done before the final values overwrite it
+        }
+        // final values into the staging rows: store v of half-warp t / 16 fills row
+        // 16 v + t / 16, each lane in the bank the plan chose (a permutation per
+        // row), so that these stores and the consumers' reads are conflict-free
+#pragma unroll
+        for (int v = 0; v < 16; ++v) ex[16 * (16 * v + (t >> 4)) + (int)((pb >> (4 * v)) & 15u)] = x[v];
       }
-      if (i + 1 < nitems) {
-        load_tile<K2>(a, ncol, ntt, t, xn);
-        pbn = __ldg(a.pbank + ntt * kNP + t);
-      }
-      phase0_stages<K2>(x);
-      if (i >= kNBuf) nbar_sync(kBarEmpty + b, NALL);  // the consumers are done with buffer b
-      double* ex = buf + (size_t)b * kE;
-      if constexpr (K2 > 4) {
-#pragma unroll
-        for (int v = 0; v < 16; ++v) ex[Geo<K2>::p0(t, v)] = x[v];
-        nbar_sync(kBarProd, kNP);
-#pragma unroll
-        for (int v = 0; v < 16; ++v) x[v] = ex[Geo<K2>::p1(t, v)];
-        phase1_stages<K2>(x);
-        nbar_sync(kBarProd, kNP);  // exchange reads done before the final values overwrite it
-      }
-      // final values into the staging rows: store v of half-warp t / 16 fills row
-      // 16 v + t / 16, each lane in the bank the plan chose (a permutation per
-      // row), so that these stores and the consumers' reads are conflict-free
-#pragma unroll
-      for (int v = 0; v < 16; ++v) ex[16 * (16 * v + (t >> 4)) + (int)((pb >> (4 * v)) & 15u)] = x[v];
       nbar_arrive(kBarFull + b, NALL);
     }
     return;
@@ -663,22 +676,23 @@ __global__ void __launch_bounds__(kNP + kNC, 1) cm_gather_kernel(const PassArgs 
     for (int q = 0; q < 6; ++q) dst[q] = bk * JB + 4 * q < J8 ? __ldg(p + q * kNC) : dq;
   };
   uint4 cw[6], nw[6];
-  double run = 0.0;  // running value of the open bucket run (it may continue into the next group of 4)
-  double* sac = sa + cls;  // this thread's bucket class: k = 16 kb + cls
+  double run[NCOL];  // running value of the open bucket run, per column
+#pragma unroll
+  for (int h = 0; h < NCOL; ++h) run[h] = 0.0;
   int Jc = nitems > 0 ? __ldg(a.hdr + 0) : 0;
   if (Jc > 0) load_block(0, 0, Jc, nw);
-  int64_t col = blockIdx.x, tt = 0;
+  int64_t grp = blockIdx.x, tt = 0;
   for (int64_t i = 0; i < nitems; ++i) {
     const int b = (int)(i % kNBuf);
     const int64_t ttn = tt + 1 == a.ntiles ? 0 : tt + 1;
     if (tt == 0) {
-      for (int k = c; k < a.nb; k += kNC) sa[k] = 0.0;
+      for (int k = c; k < NCOL * nbp; k += kNC) sa[k] = 0.0;
       nbar_sync(kBarCons, kNC);
     }
     const int Jn = i + 1 < nitems ? __ldg(a.hdr + ttn) : 0;
     const int nbk = Jc > 0 ? (Jc + JB - 1) / JB : 0;
     nbar_sync(kBarFull + b, NALL);
-    const double* tile = buf + (size_t)b * kE;
+    const double* tile = buf + (size_t)b * NCOL * kE;
     for (int bk = 0; bk < nbk; ++bk) {
 #pragma unroll
       for (int q = 0; q < 6; ++q) cw[q] = nw[q];
@@ -694,40 +708,56 @@ __global__ void __launch_bounds__(kNP + kNC, 1) cm_gather_kernel(const PassArgs 
         // register: one shared-memory read at the head, one write at the last
         // entry (the order is that of one add per entry).  Padding words are 0:
         // they read tile[0] (a broadcast) and neither load nor store the sketch.
-        double v[4], a0[4];
+        double v[NCOL][4], a0[NCOL][4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          v[u] = tile[w[u] & (kE - 1)];
-          if (w[u] & kHead) a0[u] = sac[(w[u] >> 12 & kKbMask) << 4];
+          const int p = w[u] & (kE - 1);
+          const int kk = (int)((w[u] >> 12 & kKbMask) << 4) + cls;
+#pragma unroll
+          for (int h = 0; h < NCOL; ++h) {
+            v[h][u] = tile[h * kE + p];
+            if (w[u] & kHead) a0[h][u] = sa[h * nbp + kk];
+          }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const double x = __hiloint2double(__double2hiint(v[u]) ^ (int)(w[u] & kNeg), __double2loint(v[u]));
-          run = ((w[u] & kHead) ? a0[u] : run) + x;
-          if (w[u] & kLast) sac[(w[u] >> 12 & kKbMask) << 4] = run;
+          const int kk = (int)((w[u] >> 12 & kKbMask) << 4) + cls;
+#pragma unroll
+          for (int h = 0; h < NCOL; ++h) {
+            const double x = __hiloint2double(__double2hiint(v[h][u]) ^ (int)(w[u] & kNeg), __double2loint(v[h][u]));
+            run[h] = ((w[u] & kHead) ? a0[h][u] : run[h]) + x;
+            if (w[u] & kLast) sa[h * nbp + kk] = run[h];
+          }
         }
       }
     }
     if (nbk == 0 && Jn > 0) load_block(ttn, 0, Jn, nw);
-    if (Jc < 0 && c == 0) {  // serial list (a tile whose buckets could not be balanced), ascending entry order
+    if (Jc < 0 && c < NCOL) {  // serial list (a tile whose buckets could not be balanced), ascending entry order
       const uint32_t* sl = a.words + tt * plan_tile_words(a.s);
+      double* sh = sa + c * nbp;
+      const double* th = tile + c * kE;
       for (int e = 0; e < -Jc; ++e) {
         const uint32_t x = __ldg(sl + e);
         if (!(x & kValid)) continue;
         const int k = (int)((x >> 12) & kKbMask);
-        const double vv = tile[x & (kE - 1)];
-        sa[k] = (x & kNeg) ? sa[k] - vv : sa[k] + vv;
+        const double vv = th[x & (kE - 1)];
+        sh[k] = (x & kNeg) ? sh[k] - vv : sh[k] + vv;
       }
     }
     nbar_sync(kBarCons, kNC);                                   // every add of this tile is done
     if (i + kNBuf < nitems) nbar_arrive(kBarEmpty + b, NALL);  // buffer b free (no arrival left unmatched)
-    if (tt == a.ntiles - 1 && col < a.ncols) {                  // column done: SA column out
-      double* o = col < a.ncolSA ? a.SA + col * a.ldsa : a.Sb;
-      // same k -> thread map as the zeroing above, so no barrier is needed before the next column's zeroing
-      for (int k = c; k < a.nb; k += kNC) o[a.b0 + k] = a.alpha * sa[k];
+    if (tt == a.ntiles - 1) {                                   // group done: its SA columns out
+#pragma unroll
+      for (int h = 0; h < NCOL; ++h) {
+        const int64_t col = NCOL * grp + h;
+        if (col >= a.ncols) continue;
+        double* o = col < a.ncolSA ? a.SA + col * a.ldsa : a.Sb;
+        // same k -> thread map as the zeroing above, so no barrier is needed before the next group's zeroing
+        for (int k = c; k < a.nb; k += kNC) o[a.b0 + k] = a.alpha * sa[h * nbp + k];
+      }
     }
     Jc = Jn;
-    if (ttn == 0) col += gridDim.x;
+    if (ttn == 0) grp += gridDim.x;
     tt = ttn;
   }
 }
@@ -989,17 +1019,30 @@ int launch_mid_t(const PassArgs& a, cudaStream_t st) {
   return check_launch("cm_mid");
 }
 
-template <int K2>
-int launch_gather_t(const PassArgs& a, cudaStream_t st) {
-  const size_t smem = gather_smem_bytes(a.nb);
-  auto* f = cm_gather_kernel<K2>;
+template <int K2, int NCOL>
+int launch_gather_nt(const PassArgs& a, cudaStream_t st) {
+  const size_t smem = gather_smem_bytes(a.nb, NCOL);
+  auto* f = cm_gather_kernel<K2, NCOL>;
   int rc = set_smem(f, smem);
   if (rc) return rc;
-  const int64_t grid = std::min<int64_t>(a.ncols, (int64_t)num_sms());
+  const int64_t grid = std::min<int64_t>((a.ncols + NCOL - 1) / NCOL, (int64_t)num_sms());
   if (grid < 1) return SKH_OK;
   f<<<(unsigned)grid, kNP + kNC, smem, st>>>(a);
   note_launch();
   return check_launch("cm_gather");
+}
+
+// Two columns per CTA where both sketches and staging pairs fit on chip (small
+// m) and there are columns for every SM twice over (SKH_CM_NCOL=1 turns it off)
+template <int K2>
+int launch_gather_t(const PassArgs& a, cudaStream_t st) {
+  static const bool two = [] {
+    const char* e = getenv("SKH_CM_NCOL");
+    return !(e && atoi(e) == 1);
+  }();
+  if (two && gather_smem_bytes(a.nb, 2) <= (size_t)227 * 1024 && a.ncols >= 2 * (int64_t)num_sms())
+    return launch_gather_nt<K2, 2>(a, st);
+  return launch_gather_nt<K2, 1>(a, st);
 }
 
 size_t plan_range_bytes(int64_t ntiles, int s) {

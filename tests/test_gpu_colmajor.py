@@ -161,7 +161,10 @@ def test_rht_dense_colmajor_tolerance(n, d, m, s):
 
 
 @pytest.mark.parametrize("n,d,m,s", [(2048, 24, 60, 2), (1 << 17, 3, 1000, 1), (1 << 21, 1, 7168, 1),
-                                     (50000, 4, 500, 3)])
+                                     (50000, 4, 500, 3),
+                                     # >= 2 x 148 columns and a small sketch: two columns per CTA in the
+                                     # fused pass (the odd count leaves the last CTA a dummy column)
+                                     (1 << 14, 300, 500, 1), (1 << 16, 301, 1792, 2)])
 def test_rht_dense_colmajor_integer_exact(n, d, m, s):
     """Integer inputs: every butterfly and partial sum is an exact integer, so the
     fused path equals fl(c_ns * exact integer sum) bit for bit."""
