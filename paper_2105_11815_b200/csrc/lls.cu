@@ -44,6 +44,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "common.cuh"
@@ -978,6 +979,33 @@ int form_rinv(Handles* h, int64_t d, const LlsWs& w, int64_t m, cudaStream_t st)
   return check_launch("lls: R^{-1}");
 }
 
+// Certified full rank (R22b).  Column pivoting makes the pivoted
+// diagonals non-increasing, |r~_11| >= ... >= |r~_dd|, and for any triangular
+// factor the last row of R^{-1} is e_d^T / r_dd, so |r~_dd| >= sigma_min(R0) >=
+// 1 / ||R0^{-1}||_F.  ||R0^{-1}||_F rcond <= 1/2 (a factor 2 for the rounding of
+// the computed inverse) therefore proves p = max{q : |r~_qq| >= rcond} = d
+// without pivoting: V1 = I, R11 = R0, N = R0^{-1} -- the same
+// least-squares solution as the pivoted factor (R0 = Q1 R~ P^T differs from it
+// by an orthogonal factor).  Leaves N in Ri / Rr when it returns *ok = true.
+// SKH_LLS_CPQR=1 skips the certificate (always pivot).
+int rr_certify(Handles* h, int64_t d, int64_t m, const LlsWs& w, double rcond, cudaStream_t st, bool* ok) {
+  *ok = false;
+  static const bool force = [] {
+    const char* e = getenv("SKH_LLS_CPQR");
+    return e && atoi(e) != 0;
+  }();
+  if (force || d * d >= (1ll << 31)) return SKH_OK;
+  int rc = form_rinv(h, d, w, m, st);
+  if (rc) return rc;
+  double nrm = 0.0;  // host pointer mode: the call returns when the norm is ready
+  if (cublasDnrm2(h->blas, (int)(d * d), w.Ri, 1, &nrm) != CUBLAS_STATUS_SUCCESS) {
+    set_error("lls: cublasDnrm2 (||R^{-1}||_F) failed");
+    return SKH_ECUDA;
+  }
+  *ok = std::isfinite(nrm) && nrm * rcond * 2.0 <= 1.0;
+  return SKH_OK;
+}
+
 int trsv(Handles* h, int64_t d, const LlsWs& w, int64_t m, bool trans, double* x) {
   if (w.Ri) {  // x = M x or M^T x, M = R^{-1}: one warp per row of a row-major matrix (rinv_mode)
     cudaStream_t st = nullptr;
@@ -1158,9 +1186,16 @@ static int lls_solve_impl(bool cm, int64_t n, int64_t d, const double* A, int64_
     }
   }
   int64_t p = d;
+  bool pivoted = false;
   if (rr) {
-    // rank-revealing mode: pivoted QR of R0, p from rcond, N = P [R11^{-1} 0; 0 0]
-    if ((rc = cpqr_step2(h, d, m, w, rcond, st, &p))) return rc;
+    // rank-revealing mode: p = d certified from ||R0^{-1}||_F (N = R0^{-1}), else
+    // the pivoted QR of R0, p from rcond, N = P [R11^{-1} 0; 0 0]
+    bool cert = false;
+    if ((rc = rr_certify(h, d, m, w, rcond, st, &cert))) return rc;
+    if (!cert) {
+      if ((rc = cpqr_step2(h, d, m, w, rcond, st, &p))) return rc;
+      pivoted = true;
+    }
     info[2] = p;
   } else {
     // full-rank QR mode (R19): reject a rank-deficient SA -- a diagonal entry
@@ -1190,7 +1225,7 @@ static int lls_solve_impl(bool cm, int64_t n, int64_t d, const double* A, int64_
     set_error("lls: cusolverDnDormqr failed");
     return SKH_ECUDA;
   }
-  if (rr) {  // Q^T Sb = Q1^T (Q0^T Sb): the pivoted QR's reflectors on the first d entries
+  if (pivoted) {  // Q^T Sb = Q1^T (Q0^T Sb): the pivoted QR's reflectors on the first d entries
     cpqr_qt_kernel<<<1, 256, 0, st>>>((int)d, w.Rp, w.perm, w.tau1, w.qtb);
     note_launch();
   }
