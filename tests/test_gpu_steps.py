@@ -102,3 +102,39 @@ def test_bench_col_step_integer_exact():
     SAt, Sb = run_like_bench(step)
     want, wantb = sketch.rht_sketch(seed, A, b, m, s)
     assert np.array_equal(SAt.cpu().numpy().T, want) and np.array_equal(Sb.cpu().numpy(), wantb)
+
+
+@pytest.mark.parametrize("name,layout", [("C1", "row"), ("C3", "row"), ("C4", "row"), ("C3HD", "row"),
+                                         ("C2", "col"), ("C5", "col")])
+def test_bench_step_graph_replay(name, layout):
+    """bench.py times short steps as replays of the step captured in a CUDA
+    graph (bench.capture_step): every replay redraws S and recomputes SA, Sb.
+    Replays after the inputs change must give the oracle's sketch of the NEW
+    inputs (nothing cached), bit-identical for the row-major paths and to
+    1e-12 for the fused column-major one (R17)."""
+    import bench
+    from oracle import sketch
+    from synth import configs, gen
+    cfg = configs.ALL[name].scaled(**REPLICAS[name])
+    step, inputs = bench.build_step(cfg, torch, layout)
+    g, per_step = bench.capture_step(step, torch)
+    assert per_step > 0
+    if cfg.kind == "csr":
+        rp, ci, v = gen.csr(cfg)
+        inputs[2].mul_(-2.0)  # new values in place; the captured pointers stay valid
+        want, wantb = sketch.sketch_csr(cfg.seed, rp, ci, -2.0 * v, cfg.d, gen.rhs(cfg), cfg.m, cfg.s)
+    else:
+        inputs[0].mul_(-2.0)
+        A = -2.0 * gen.dense(cfg)
+        want, wantb = (sketch.rht_sketch if cfg.hd else sketch.sketch_dense)(cfg.seed, A, gen.rhs(cfg), cfg.m, cfg.s)
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    out = step.SAt if layout == "col" else step.SA
+    got, gotb = out.cpu().numpy(), step.Sb.cpu().numpy()
+    if layout == "col":
+        got = got.T
+        assert np.linalg.norm(got - want) <= TOL * np.linalg.norm(want)
+        assert np.linalg.norm(gotb - wantb) <= TOL * np.linalg.norm(wantb)
+    else:
+        assert np.array_equal(got, want) and np.array_equal(gotb, wantb)
