@@ -9,18 +9,20 @@ import sys
 
 # bench stage -> kernels it launches (name prefixes; summed per launch of the stage)
 STAGES = {
-    "C5-col": {"pass1": ["cm_pass1p_kernel"], "pass2_gather": ["cm_gather_kernel"]},
+    "C5-col": {"pass1": ["cm_pass1"], "pass2_gather": ["cm_gather_kernel"]},
     "C5-row": {"fwht_pass0": ["fwht_tile_kernel<7, 1>"], "fwht_pass1": ["fwht_tile_kernel<7, 0>"],
                "fwht_pass2": ["fwht_tile_kernel<7, 0>"], "gather": ["gather_wide_kernel"]},
+    "C2-col": {"pass1": ["cm_pass1"], "pass2_gather": ["cm_gather_kernel"]},
     "C2-row": {"fwht_pass0": ["fwht_tile_kernel<8, 1>"], "fwht_pass1": ["fwht_tile_kernel<8, 0>"],
                "gather": ["gather_wide_kernel"]},
     "C3HD-row": {"fwht_pass0": ["fwht_tile_kernel<9, 1>"], "fwht_pass1": ["fwht_tile_kernel<8, 0>"],
                  "gather": ["gather_group_kernel"]},
     "C3-row": {"gather": ["gather_group_kernel"]},
     "C4-row": {"gather_csr": ["csr_len_kernel", "csr_expand_kernel", "csr_reduce_kernel"]},
+    "C1-row": {"gather": ["gather_dense_kernel"]},
 }
-FILES = {"C5-col": "C5_auto", "C5-row": "C5_row", "C2-row": "C2_auto", "C3HD-row": "C3HD_auto", "C3-row": "C3_auto",
-         "C4-row": "C4_auto"}
+FILES = {"C5-col": "C5_auto", "C5-row": "C5_row", "C2-col": "C2_auto", "C2-row": "C2_row", "C3HD-row": "C3HD_auto",
+         "C3-row": "C3_auto", "C4-row": "C4_auto", "C1-row": "C1_auto"}
 
 
 def launches(path):
