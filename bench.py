@@ -417,7 +417,11 @@ def time_step(step, steps, torch, graph=True):
     stage_ms = {k: sum(p[k] for p in per) / len(per) for k in per[0]}
     if not graph or ms_eager > GRAPH_MAX_MS:
         return ms_eager, stage_ms, launches, "eager", ms_eager
-    g, per_step = capture_step(step, torch)
+    try:
+        g, per_step = capture_step(step, torch)
+    except RuntimeError as e:  # a step that cannot be captured is timed eagerly
+        torch.cuda.synchronize()
+        return ms_eager, stage_ms, launches, f"eager (graph capture failed: {str(e)[:80]})", ms_eager
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -484,6 +488,7 @@ def gpu_arm_single(args, cfg):
         line["cpu_baseline"] = cpu_line
     if args.sketch == "hashing" and not args.no_all_workloads:
         line["workloads"] = other_workloads_measure(args, cfg, torch, pk, src)
+        line["next_rows"] = next_rows_measure(args, torch, pk)
     print(json.dumps(line), flush=True)
 
 
@@ -520,6 +525,57 @@ def other_workloads_measure(args, main_cfg, torch, pk, src):
         out[name] = rec
         del step, inputs
         torch.cuda.empty_cache()
+    return out
+
+
+def next_rows_measure(args, torch, pk):
+    """SURVEY §8(f) "next" rows on C2 in the same run (driver-measured): NEXT-1
+    Algorithm 1 Steps 2-5 (the paper's default rank-revealing Step 2, rcond
+    1e-12, then LSQR to the (7.1) stop) on the timed step's SA, Sb; NEXT-2 the
+    s-hashing variant sketch; NEXT-3 HR-DHT and NEXT-4 SR-DHT sketches.  Each
+    sketch: W warm-up + min(K, 10) timed steps (CUDA-graph replays, as above);
+    the solve: one warm-up and one timed call with the library's stage trace."""
+    import paper_2105_11815_b200 as skh
+    from synth import configs
+    cfg = configs.ALL["C2"]
+    out = {"workload": cfg.name}
+    steps = max(1, min(args.steps, 10))
+    for key, sk in (("next2_variant", "variant"), ("next3_hrdht", "dht"), ("next4_srdht", "srdht")):
+        step, inputs = build_step(cfg, torch, "row", sk)
+        for _ in range(max(args.warmup, 0)):
+            step.run()
+        ms, stage_ms, _, mode, ms_eager = time_step(step, steps, torch, not args.no_graph)
+        out[key] = {"ms_per_step": round(ms, 4), "launch": mode, "ms_per_step_eager": round(ms_eager, 4),
+                    "value": round(cfg.a_bytes / (ms / 1e3) / 1e9, 2), "unit": "GB/s",
+                    "alg_frac": round(alg_bytes_step(cfg, cfg.n) / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4),
+                    "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()}}
+        del step, inputs
+        torch.cuda.empty_cache()
+    step, (A, b) = build_step(cfg, torch, "row")
+    SA, Sb = step.run()
+    SA, Sb = SA.clone(), Sb.clone()
+    del step
+    solver = skh.LlsSolver(cfg.n, cfg.d, cfg.m, rcond=1e-12)
+    solver(A, b, SA, Sb)  # warm-up: handles, cuSOLVER workspace
+    torch.cuda.synchronize()
+    with skh.Trace(16) as tr:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        x, info = solver(A, b, SA, Sb)
+        e1.record()
+    torch.cuda.synchronize()
+    st = tr.durations_ms()
+    it = max(info["iters"], 1)
+    per_it = st.get("lsqr", 0.0) / it
+    gbs = 2 * cfg.a_bytes / (per_it / 1e3) / 1e9 if per_it > 0 else None
+    out["next1_solve"] = {"ms": round(e0.elapsed_time(e1), 3), "step2": "rank-revealing (rcond 1e-12)",
+                          "rank": info["rank"], "iters": info["iters"], "stop_test2": info["test2"],
+                          "exit_step": info["step"], "stages_ms": {k: round(v, 3) for k, v in st.items()},
+                          "ms_per_lsqr_iter": round(per_it, 4),
+                          "lsqr_A_frac": (round(gbs / pk["hbm_gbs"], 3) if gbs else None),
+                          "note": "each LSQR iteration reads A twice (A R^-1 v, A^T u)"}
+    del A, b, SA, Sb, x, solver
+    torch.cuda.empty_cache()
     return out
 
 
