@@ -613,6 +613,50 @@ __global__ void __launch_bounds__(kNP + kNC, 1) cm_gather_kernel(const PassArgs 
   const int64_t ngroups = (a.ncols + NCOL - 1) / NCOL;
   const int64_t my_groups = ngroups > blockIdx.x ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t nitems = my_groups * a.ntiles;
+  if (tid < kNP && K2 <= 4) {
+    // no exchange (K2 <= 4): two register tiles with alternating roles (the loop
+    // is unrolled by two), so the tile in flight is never copied into the one
+    // being transformed (same-box A/B: C3HD pass 2 2.248 -> 2.216 ms, C2 unchanged;
+    // with the exchange the doubled producer code measured slower on C5, so
+    // K2 > 4 keeps the copy)
+    const int t = tid;
+    double xa[16], xb[16];
+    uint64_t pba = 0, pbb = 0;
+    int64_t ngrp = blockIdx.x, ntt = 0;  // the (group, tile) of the loads in flight
+    int nh = 0;                          // ... and which column of the group
+    const int64_t nq = nitems * NCOL;    // (item, column) steps
+    if (nq > 0) {
+      load_tile<K2>(a, NCOL * ngrp, ntt, t, xa);
+      pba = __ldg(a.pbank + ntt * kNP + t);
+    }
+    auto step = [&](int64_t q, double (&x)[16], uint64_t pb, double (&xn)[16], uint64_t& pbn) {
+      const int64_t i = q / NCOL;
+      const int h = (int)(q - i * NCOL);
+      const int b = (int)(i % kNBuf);
+      if (++nh == NCOL) {
+        nh = 0;
+        if (++ntt == a.ntiles) {
+          ntt = 0;
+          ngrp += gridDim.x;
+        }
+      }
+      if (q + 1 < nq) {
+        load_tile<K2>(a, NCOL * ngrp + nh, ntt, t, xn);
+        pbn = __ldg(a.pbank + ntt * kNP + t);
+      }
+      phase0_stages<K2>(x);
+      if (h == 0 && i >= kNBuf) nbar_sync(kBarEmpty + b, NALL);
+      double* ex = buf + ((size_t)b * NCOL + h) * kE;
+#pragma unroll
+      for (int v = 0; v < 16; ++v) ex[16 * (16 * v + (t >> 4)) + (int)((pb >> (4 * v)) & 15u)] = x[v];
+      if (h == NCOL - 1) nbar_arrive(kBarFull + b, NALL);
+    };
+    for (int64_t q = 0; q < nq; q += 2) {
+      step(q, xa, pba, xb, pbb);
+      if (q + 1 < nq) step(q + 1, xb, pbb, xa, pba);
+    }
+    return;
+  }
   if (tid < kNP) {
     const int t = tid;
     double x[16], xn[16];
