@@ -39,6 +39,17 @@ def _ld(t):
     return t.stride(0) if t.size(0) > 1 else max(t.size(1), 1)
 
 
+def _check_out(t, shape, name):
+    """A caller-given output buffer: a CUDA float64 tensor of the output's shape
+    (1-D outputs: the right number of elements), since the C ABI only sees a
+    pointer and a leading dimension."""
+    if not t.is_cuda or t.dtype != torch.float64:
+        raise ValueError(f"{name} must be a CUDA float64 tensor")
+    ok = t.numel() == shape[0] if len(shape) == 1 else tuple(t.shape) == tuple(shape)
+    if not ok:
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
 def _workspace(nbytes, device):
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 
@@ -84,6 +95,13 @@ def hash_gen(seed, m, s, nrows, row0=0, blk=0, stride=0, want_cols=False, device
             out.col_rows = torch.empty(max(N, 1), dtype=torch.int32, device=device)
             out.col_signs = torch.empty(max(N, 1), dtype=torch.int8, device=device)
         out.ws = _workspace(lib.skh_hash_workspace_bytes(nrows, m, s), device)
+    elif (out.ptr.numel() < m + 1 or out.rows.numel() < N or out.signs.numel() < N
+          or (out.col_rows is not None and out.col_rows.numel() < N)
+          or (out.col_signs is not None and out.col_signs.numel() < N)):
+        raise ValueError(f"hash_gen: out holds lists for m={out.m}, s={out.s}, nrows={out.nrows}; "
+                         f"asked for m={m}, s={s}, nrows={nrows}")
+    else:
+        out.m, out.s, out.nrows = int(m), int(s), int(nrows)
     fn = lib.skh_hash_gen_variant if variant else lib.skh_hash_gen
     rc = fn(int(seed) & (2**64 - 1), int(m), int(s), int(nrows), int(row0), int(blk), int(stride),
             _ptr(out.col_rows), _ptr(out.col_signs), _ptr(out.ptr), _ptr(out.rows), _ptr(out.signs),
@@ -106,8 +124,12 @@ def sketch_dense(bl, A, b=None, alpha=None, SA=None, Sb=None):
     n, d = A.shape
     if SA is None:
         SA = torch.empty(bl.m, d, dtype=torch.float64, device=A.device)
+    else:
+        _check_out(SA, (bl.m, d), "SA")
     if b is not None and Sb is None:
         Sb = torch.empty(bl.m, dtype=torch.float64, device=A.device)
+    elif b is not None:
+        _check_out(Sb, (bl.m,), "Sb")
     alpha = c_s(bl.s) if alpha is None else float(alpha)
     rc = lib.skh_sketch_dense(bl.m, bl.s, _ptr(bl.ptr), _ptr(bl.rows), _ptr(bl.signs), n, d, _ptr(A), _ld(A),
                               _ptr(b), _ptr(SA), _ld(SA), _ptr(Sb), alpha, _stream())
@@ -130,8 +152,12 @@ def sketch_csr(bl, row_ptr, col_idx, val, d, b=None, alpha=None, SA=None, Sb=Non
     dev = row_ptr.device
     if SA is None:
         SA = torch.empty(bl.m, d, dtype=torch.float64, device=dev)
+    else:
+        _check_out(SA, (bl.m, d), "SA")
     if b is not None and Sb is None:
         Sb = torch.empty(bl.m, dtype=torch.float64, device=dev)
+    elif b is not None:
+        _check_out(Sb, (bl.m,), "Sb")
     if ws is None:
         ws = sketch_csr_workspace(n, bl.s, nnz, dev)
     alpha = c_s(bl.s) if alpha is None else float(alpha)
@@ -175,6 +201,8 @@ def rht_stages(seed, X, bit_lo, bit_hi, nrows=None, row0=0, apply_diag=True, alp
     nrows = nvalid if nrows is None else int(nrows)
     if Y is None:
         Y = torch.empty(nrows, d, dtype=torch.float64, device=X.device)
+    else:
+        _check_out(Y, (nrows, d), "Y")
     if ws is None:
         ws = rht_stages_workspace(nrows, nvalid, row0, d, X.device)
     rc = lib.skh_rht_stages(int(seed) & (2**64 - 1), nrows, nvalid, int(row0), d, _ptr(X), _ld(X), _ptr(Y), _ld(Y),
@@ -198,8 +226,12 @@ class RhtDense:
         _need_cuda(A, b)
         if SA is None:
             SA = torch.empty(self.m, self.d, dtype=torch.float64, device=A.device)
+        else:
+            _check_out(SA, (self.m, self.d), "SA")
         if b is not None and Sb is None:
             Sb = torch.empty(self.m, dtype=torch.float64, device=A.device)
+        elif b is not None:
+            _check_out(Sb, (self.m,), "Sb")
         rc = lib.skh_rht_dense(int(seed) & (2**64 - 1), self.n, self.m, self.s, self.d, _ptr(A), _ld(A), _ptr(b),
                                _ptr(SA), _ld(SA), _ptr(Sb), _ptr(self.ws), self.ws.numel(), _stream())
         _lib.check(rc, "skh_rht_dense")
@@ -331,8 +363,12 @@ class RhtColMajorLists:
             raise ValueError(f"At must be float64 of shape (d, L) = ({self.d}, {self.L})")
         if SAt is None:
             SAt = torch.empty(self.d, self.m, dtype=torch.float64, device=At.device)
+        else:
+            _check_out(SAt, (self.d, self.m), "SAt")
         if b is not None and Sb is None:
             Sb = torch.empty(self.m, dtype=torch.float64, device=At.device)
+        elif b is not None:
+            _check_out(Sb, (self.m,), "Sb")
         rc = lib.skh_rht_colmajor_lists(int(seed) & (2**64 - 1), self.L, int(row0), self.m, self.s_eff, self.d,
                                         _ptr(At), _ld_cm(At, self.L), _ptr(b), _ptr(col_rows), _ptr(col_signs),
                                         float(alpha), _ptr(SAt), _ld_cm(SAt, self.m), _ptr(Sb), _ptr(self.ws),
@@ -358,8 +394,12 @@ class RhtDenseColMajor:
             raise ValueError(f"At must be float64 of shape (d, n) = ({self.d}, {self.n})")
         if SAt is None:
             SAt = torch.empty(self.d, self.m, dtype=torch.float64, device=At.device)
+        else:
+            _check_out(SAt, (self.d, self.m), "SAt")
         if b is not None and Sb is None:
             Sb = torch.empty(self.m, dtype=torch.float64, device=At.device)
+        elif b is not None:
+            _check_out(Sb, (self.m,), "Sb")
         rc = lib.skh_rht_dense_colmajor(int(seed) & (2**64 - 1), self.n, self.m, self.s, self.d, _ptr(At),
                                         _ld_cm(At, self.n), _ptr(b), _ptr(SAt), _ld_cm(SAt, self.m), _ptr(Sb),
                                         _ptr(self.ws), self.ws.numel(), _stream())
@@ -399,8 +439,12 @@ def sketch_dense_colmajor(seed, At, b, m, s, SAt=None, Sb=None, ws=None, fast=Tr
     d, n = At.shape
     if SAt is None:
         SAt = torch.empty(d, m, dtype=torch.float64, device=At.device)
+    else:
+        _check_out(SAt, (d, m), "SAt")
     if b is not None and Sb is None:
         Sb = torch.empty(m, dtype=torch.float64, device=At.device)
+    elif b is not None:
+        _check_out(Sb, (m,), "Sb")
     if ws is None:
         nb = (lib.skh_sketch_dense_colmajor_fast_workspace_bytes(n, m, s, d) if fast
               else lib.skh_sketch_dense_colmajor_workspace_bytes(n, m, s))
@@ -534,8 +578,12 @@ def hrdht_dense(seed, A, b, m, s, SA=None, Sb=None, ws=None):
     n, d = A.shape
     if SA is None:
         SA = torch.empty(m, d, dtype=torch.float64, device=A.device)
+    else:
+        _check_out(SA, (m, d), "SA")
     if b is not None and Sb is None:
         Sb = torch.empty(m, dtype=torch.float64, device=A.device)
+    elif b is not None:
+        _check_out(Sb, (m,), "Sb")
     if ws is None:
         nb = lib.skh_hrdht_dense_workspace_bytes(n, int(m), int(s), d)
         if nb == 0:
@@ -554,8 +602,12 @@ def hrdht_dense_colmajor(seed, At, b, m, s, SAt=None, Sb=None, ws=None):
     d, n = At.shape
     if SAt is None:
         SAt = torch.empty(d, m, dtype=torch.float64, device=At.device)
+    else:
+        _check_out(SAt, (d, m), "SAt")
     if b is not None and Sb is None:
         Sb = torch.empty(m, dtype=torch.float64, device=At.device)
+    elif b is not None:
+        _check_out(Sb, (m,), "Sb")
     if ws is None:
         nb = lib.skh_hrdht_dense_colmajor_workspace_bytes(n, int(m), int(s), d)
         if nb == 0:
@@ -574,8 +626,12 @@ def srdht_dense(seed, A, b, m, SA=None, Sb=None, ws=None):
     n, d = A.shape
     if SA is None:
         SA = torch.empty(m, d, dtype=torch.float64, device=A.device)
+    else:
+        _check_out(SA, (m, d), "SA")
     if b is not None and Sb is None:
         Sb = torch.empty(m, dtype=torch.float64, device=A.device)
+    elif b is not None:
+        _check_out(Sb, (m,), "Sb")
     if ws is None:
         nb = lib.skh_srdht_dense_workspace_bytes(n, int(m), d)
         if nb == 0:

@@ -132,3 +132,33 @@ def test_error_codes_widened_entry_points(lib):
                              None) == EINVAL
     assert lib.skh_trace_set(None, -1) == EINVAL
     assert lib.skh_trace_set(None, 0) == 0 and lib.skh_trace_count() == 0
+
+
+def test_binding_rejects_mis_sized_outputs():
+    """The binding checks caller-given output buffers (the C ABI sees only a
+    pointer and a leading dimension): a CPU tensor, a wrong dtype or a wrong
+    shape raises before any library call."""
+    import torch
+
+    from paper_2105_11815_b200 import api
+    with pytest.raises(ValueError, match="CUDA float64"):
+        api._check_out(torch.zeros(4, 3, dtype=torch.float64), (4, 3), "SA")
+    with pytest.raises(ValueError, match="CUDA float64"):
+        api._check_out(torch.zeros(4, 3, dtype=torch.float32), (4, 3), "SA")
+
+
+@pytest.mark.gpu
+def test_binding_rejects_mis_sized_outputs_gpu():
+    import torch
+
+    from paper_2105_11815_b200 import api
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    A = torch.zeros(64, 8, dtype=torch.float64, device="cuda")
+    bl = api.hash_gen(1, 16, 2, 64)
+    with pytest.raises(ValueError, match="shape"):
+        api.sketch_dense(bl, A, SA=torch.zeros(16, 7, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError, match="out holds lists"):
+        api.hash_gen(1, 16, 2, 65, out=bl)
+    SA, _ = api.sketch_dense(bl, A, SA=torch.zeros(16, 8, dtype=torch.float64, device="cuda"))
+    assert SA.shape == (16, 8)
