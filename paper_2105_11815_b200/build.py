@@ -16,6 +16,11 @@ PKG = os.path.join(ROOT, "paper_2105_11815_b200")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+# SKH_CHECKED=1: the checked build (device-side SKH_CHECK invariants, common.cuh);
+# always a full rebuild, and the next plain build rebuilds again
+CHECKED = os.environ.get("SKH_CHECKED", "0") == "1"
+if CHECKED:
+    FLAGS = FLAGS + ["-DSKH_CHECKED"]
 
 TARGETS = {
     os.path.join(PKG, "libskh.so"): sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu"))),
@@ -59,8 +64,11 @@ def build(force=False, verbose=False):
     for out, srcs in TARGETS.items():
         if not srcs:
             continue
-        if not force and not _stale(out, srcs):
+        stamp = out + ".checked"
+        was_checked = os.path.exists(stamp)
+        if not force and not _stale(out, srcs) and was_checked == CHECKED:
             continue
+        force = force or was_checked != CHECKED
         objdir = os.path.join(os.path.dirname(out), "build_obj")
         os.makedirs(objdir, exist_ok=True)
         objs = [os.path.join(objdir, os.path.basename(s).replace(".cu", ".o")) for s in srcs]
@@ -73,6 +81,10 @@ def build(force=False, verbose=False):
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"link failed for {out}")
+        if CHECKED:
+            open(stamp, "w").close()
+        elif os.path.exists(stamp):
+            os.remove(stamp)
         built.append(out)
     return built
 

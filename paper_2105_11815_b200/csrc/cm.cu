@@ -757,6 +757,7 @@ __global__ void __launch_bounds__(kNP + kNC, 1) cm_gather_kernel(const PassArgs 
         for (int u = 0; u < 4; ++u) {
           const int p = w[u] & (kE - 1);
           const int kk = (int)((w[u] >> 12 & kKbMask) << 4) + cls;
+          SKH_CHECK(kk < nbp);
 #pragma unroll
           for (int h = 0; h < NCOL; ++h) {
             v[h][u] = tile[h * kE + p];
@@ -784,6 +785,7 @@ __global__ void __launch_bounds__(kNP + kNC, 1) cm_gather_kernel(const PassArgs 
         const uint32_t x = __ldg(sl + e);
         if (!(x & kValid)) continue;
         const int k = (int)((x >> 12) & kKbMask);
+        SKH_CHECK(k < a.nb);
         const double vv = th[x & (kE - 1)];
         sh[k] = (x & kNeg) ? sh[k] - vv : sh[k] + vv;
       }
@@ -910,6 +912,7 @@ __global__ void __launch_bounds__(256) cm_plan_kernel(const int32_t* __restrict_
     entry(e, k, neg);
     if (k >= 0) {
       const int pos = atomicAdd(&off[(k & 15) * nkb + (k >> 4)], 1);
+      SKH_CHECK(pos >= 0 && pos < E);
       sorted[pos] = (uint32_t)e | ((uint32_t)(k >> 4) << 15) | ((uint32_t)neg << 31);
     }
   }

@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "../../include/skh.h"
 
@@ -31,6 +32,26 @@ __host__ __device__ __forceinline__ uint64_t stream_u(uint64_t key, uint64_t ctr
 
 __host__ __device__ __forceinline__ uint64_t key_hash(uint64_t seed) { return mix64(seed ^ kLabelHash); }
 __host__ __device__ __forceinline__ uint64_t key_diag(uint64_t seed) { return mix64(seed ^ kLabelDiag); }
+
+// SKH_CHECK: device-side invariant checks of the checked build (SKH_CHECKED=1
+// python -m paper_2105_11815_b200.build --force; tools/checked_suite.sh) --
+// the stand-in for compute-sanitizer, which is closed on the GPU pool.  A
+// failed check prints its location and traps (the launch fails, the caller
+// gets SKH_ECUDA); the product build compiles them out.
+#ifdef SKH_CHECKED
+#define SKH_CHECK(c)                                                                     \
+  do {                                                                                   \
+    if (!(c)) {                                                                          \
+      printf("SKH_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             (int)blockIdx.x, (int)threadIdx.x);                                         \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define SKH_CHECK(c) \
+  do {               \
+  } while (0)
+#endif
 
 // Local column k -> global column of S (see skh_hash_gen).
 __host__ __device__ __forceinline__ int64_t row_map(int64_t k, int64_t row0, int64_t blk, int64_t stride) {

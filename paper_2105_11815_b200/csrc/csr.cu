@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 4) csr_reduce_kernel(
   __shared__ int side_n, fallback;
   const int64_t b = blockIdx.x;
   const int e_beg = off[ptr[b]], e_end = off[ptr[b + 1]];
+  SKH_CHECK(0 <= e_beg && e_beg <= e_end);
   const int ntiles = (int)((d + tile_cols - 1) / tile_cols);
   const bool whole = e_end - e_beg <= kChunk;
   int pcol[kPer];

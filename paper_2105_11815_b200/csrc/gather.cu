@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kWarps * 32) gather_dense_kernel(
   const bool va = ca < d, vb = cb < d;
   double acc0 = 0.0, acc1 = 0.0;
   const int beg = ptr[b], end = ptr[b + 1];
+  SKH_CHECK(0 <= beg && beg <= end);
   for (int t0 = beg; t0 < end; t0 += 32) {
     const int cnt = min(32, end - t0);
     int my_row = 0, my_neg = 0;
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(kWarps * 32) gather_wide_kernel(
   const bool va = ca < d, vb = cb < d;  // d even: pairs are whole
   double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
   const int beg = ptr[b], end = ptr[b + 1];
+  SKH_CHECK(0 <= beg && beg <= end);
   for (int t0 = beg; t0 < end; t0 += 32) {
     const int cnt = min(32, end - t0);
     int my_row = 0, my_neg = 0;
@@ -178,6 +180,7 @@ __global__ void __launch_bounds__(kWarps * 32) gather_group_kernel(
   const bool va = live && ca < d, vb = live && cb < d;  // d even: pairs are whole
   double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
   const int beg = live ? ptr[b] : 0, end = live ? ptr[b + 1] : 0;
+  SKH_CHECK(0 <= beg && beg <= end);
   const int len = end - beg;
   int lmax = len;  // the warp runs the longest bucket's trips
 #pragma unroll
@@ -230,6 +233,7 @@ __global__ void gather_vec_kernel(int64_t m, const int32_t* __restrict__ ptr, co
   const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (b >= m) return;
   const int beg = ptr[b], end = ptr[b + 1];
+  SKH_CHECK(0 <= beg && beg <= end);
   double acc = 0.0;
   for (int t0 = beg; t0 < end; t0 += 32 * kU) {
     int r[kU];

@@ -289,6 +289,7 @@ __global__ void finalize_kernel(const uint64_t* __restrict__ keys, int64_t N, in
   if (t >= N) return;
   const uint64_t key = keys[t];
   const int64_t b = (int64_t)(key >> 32);
+  SKH_CHECK(b < m && (t == 0 || (int64_t)(keys[t - 1] >> 32) <= b));  // sorted bucket ids in [0, m)
   const uint32_t lo = (uint32_t)key;
   bucket_rows[t] = (int32_t)(lo >> 1);
   bucket_signs[t] = (lo & 1u) ? (int8_t)-1 : (int8_t)1;
