@@ -305,6 +305,16 @@ def roofline(cfg, step, stage_ms, ms_step, peak_gbs, peak_src, layout="row", ske
         if all(k in kt for k in present):
             step_traffic = sum(kt[k]["dram_bytes_per_launch"] * table[k][2] for k in present)
     ach_step = alg_step / (ms_step / 1e3) / 1e9
+    per_kernel = {}
+    for st, (kn, al, nl_) in table.items():
+        if st not in present or present[st] <= 0:
+            continue
+        tl = present[st] / nl_
+        a_ = al / (tl / 1e3) / 1e9
+        tr = rec.get("kernels", {}).get(st, {}).get("dram_bytes_per_launch") if rec else None
+        per_kernel[st] = {"kernel": kn, "ms_per_launch": round(tl, 4), "achieved": round(a_, 1),
+                          "frac": round(a_ / peak_gbs, 4), "traffic": tr,
+                          "dram_frac": (round(tr / (tl / 1e3) / 1e9 / peak_gbs, 4) if tr else None)}
     out = {"bound": "hbm", "kernel": kern, "stage": name, "achieved": round(achieved, 1), "peak": peak_gbs,
            "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": traffic,
            "alg_bytes_per_launch": alg, "ms_per_launch": round(t_launch, 4), "peak_source": peak_src,
@@ -316,7 +326,8 @@ def roofline(cfg, step, stage_ms, ms_step, peak_gbs, peak_src, layout="row", ske
                     "alg_frac_of_8tbs_spec": round(ach_step / SPEC_HBM_GBS, 4), "traffic": step_traffic,
                     "traffic_ratio": (round(step_traffic / alg_step, 3) if step_traffic else None),
                     "note": "SURVEY §8(d): |A| + |b| + |SA| + |Sb| + s*5 B of lists per hashed row, over the "
-                            "step time"}}
+                            "step time"},
+           "per_kernel": per_kernel}
     return out
 
 
