@@ -401,7 +401,8 @@ def capture_step(step, torch):
     return g, per_step
 
 
-GRAPH_MAX_MS = 5.0  # longer steps (C5: 15 launches in 45 ms) gain nothing from a graph
+GRAPH_MAX_MS = 2.0  # longer steps gain nothing from a graph (C5: 15 launches in 45 ms; C3HD 3.7 ms:
+#                     its side-stream branch replayed 3.75 vs 3.65-3.69 ms eager)
 
 
 def time_step(step, steps, torch, graph=True):
@@ -410,7 +411,7 @@ def time_step(step, steps, torch, graph=True):
     taken over K replays of the step captured as one CUDA graph (launch
     overhead off the critical path: C1 0.067 -> 0.027 ms, C4 0.72 -> 0.68 ms),
     or from the eager pass itself with graph=False or a step longer than
-    GRAPH_MAX_MS.  Returns (ms per step,
+    GRAPH_MAX_MS (not launch-bound).  Returns (ms per step,
     stage ms, kernels launched in the timed region, mode, eager ms per step)."""
     import paper_2105_11815_b200 as skh
     timers = [step.new_timer() for _ in range(steps)]
