@@ -88,9 +88,10 @@ __host__ __device__ constexpr int tile_threads() {
 
 // Fast pass: K in [4, 11]; X/Y 16-byte aligned, even ld, even d.
 template <int K, bool DIAG>
-// K = 9 (three register phases) is capped at 80 registers so three CTAs fit per
-// SM: C3HD pass 0 1.47 -> 1.42 ms (same-box A/B, `profiles/r02/ab_tile9_occupancy.log`)
-__global__ void __launch_bounds__(tile_threads<K>(), K == 9 ? 3 : 1) fwht_tile_kernel(
+// K = 7..9 are capped at 80 registers so three CTAs fit per SM (same-box A/Bs,
+// `profiles/r02/ab_tile9_occupancy.log`, `ab_tile789_occupancy.log`): C3HD pass 0
+// 1.47 -> 1.42 ms, pass 1 1.349 -> 1.337; C5 row-major passes -1.3 %
+__global__ void __launch_bounds__(tile_threads<K>(), K >= 7 && K <= 9 ? 3 : 1) fwht_tile_kernel(
     const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy, int64_t nvalid, int lo,
     int64_t d, int64_t ntc, int64_t g_begin, uint64_t dkey, int64_t row0, double alpha) {
   constexpr int TC = tile_cols<K>();
